@@ -1,0 +1,124 @@
+/*
+ * ht_stage2.h -- C ABI of the B200-native stage-two Hessenberg-triangular
+ * reduction (arxiv 2301.07964, "ParaHT").
+ *
+ * Operation (problem statement, r-HT form;
+ * PAPER.md:1813-1841, Alg. 2 contract "REQUIRE n x n pencil (A,B) in
+ * r-Hessenberg-triangular form, ENSURE (A_orig,B_orig) = Q(A,B)Z^* with (A,B)
+ * in Hessenberg-triangular form"):
+ *
+ *   Input  (H, T): n x n, H(i,j) = 0 for i > j + r, T(i,j) = 0 for i > j.
+ *   Output (H, T): H upper Hessenberg, T upper triangular, with every entry
+ *          below H's first subdiagonal and below T's diagonal EXACTLY 0.0,
+ *          and  Q <- Q_in Q2,  Z <- Z_in Z2  where (H_in,T_in) = Q2 (H_out,T_out) Z2^*.
+ *          Q2 e1 = Z2 e1 = e1.  (LAPACK COMPQ='V' / COMPZ='V' semantics.)
+ *
+ * Layout: column-major; element (i,j) (0-based) at p[i + j*ld]; ld >= max(1,n).
+ * All matrix pointers are DEVICE pointers on the calling thread's current
+ * CUDA device (cudaSetDevice before the call).
+ *
+ * Ownership: the caller owns all buffers; the update is in place.  Workspace
+ * is allocated stream-ordered on `stream` (cudaMallocAsync) and freed before
+ * return; no pointer is retained after return.
+ *
+ * Streams: stream-ordered on `stream` (like cuSOLVER).  Internal streams are
+ * joined back to `stream` with events.  The host blocks once at entry (input
+ * validation) and may block at exit.
+ *
+ * Q == NULL or Z == NULL skips that accumulation; H and T are then bitwise
+ * identical to an accumulating run.
+ *
+ * Multi-GPU (comm != NULL): SPMD -- every rank calls the same function with
+ * its own full-size buffers holding identical inputs; on return the result
+ * is valid on opts->root (default 0); other ranks' Q/Z buffers are clobbered.
+ *
+ * Return codes (LAPACK INFO style):
+ *    0  success
+ *   -i  argument i invalid (1-based position: n < 0, r < 0, null H/T,
+ *       ld < max(1,n)); returned synchronously, nothing launched
+ *    1  input violates the r-HT structure (nonzero below H's r-th subdiagonal
+ *       or below T's diagonal) -- checked exactly on the device before work
+ *    2  input has a non-finite entry (NaN/Inf) in H, T, Q or Z
+ *    3  CUDA error   4  NCCL error   5  out of device memory
+ * No partial results are promised on error.
+ *
+ * Trivial cases: n <= 2 or r <= 1 is an exact no-op.  r >= n-1 is allowed.
+ */
+#ifndef HT_STAGE2_H
+#define HT_STAGE2_H
+
+#include <stdint.h>
+#include <cuda_runtime_api.h>
+#include <cuComplex.h>
+
+#ifndef NCCL_H_
+struct ncclComm;
+typedef struct ncclComm *ncclComm_t;
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Tunables (NULL = defaults).  q: sweeps per group ("q");
+ * 0 = default (environment HT_Q, else a per-r choice documented in DESIGN.md).
+ * chase_ctas: CTAs of the wavefront chase kernel (0 = min(q, 32)).
+ * root: result rank for comm != NULL.  flags: bit 0 = skip input validation. */
+typedef struct ht_opts {
+    int64_t q;
+    int32_t chase_ctas;
+    int32_t root;
+    int32_t flags;
+    int32_t reserved[5];
+} ht_opts;
+
+#define HT_FLAG_NO_VALIDATE 1
+
+/* Real FP64 stage two.  Arguments 1..12 in order: n, r, H, ldh, T, ldt,
+ * Q, ldq, Z, ldz, stream, comm. */
+int ht_stage2_d(int64_t n, int64_t r, double *H, int64_t ldh, double *T, int64_t ldt,
+                double *Q, int64_t ldq, double *Z, int64_t ldz, cudaStream_t stream,
+                ncclComm_t comm);
+
+/* Complex FP64 stage two (conjugate transposes throughout; reading c2). */
+int ht_stage2_z(int64_t n, int64_t r, cuDoubleComplex *H, int64_t ldh, cuDoubleComplex *T,
+                int64_t ldt, cuDoubleComplex *Q, int64_t ldq, cuDoubleComplex *Z, int64_t ldz,
+                cudaStream_t stream, ncclComm_t comm);
+
+/* Same as above with options (argument 13). */
+int ht_stage2_d_ex(int64_t n, int64_t r, double *H, int64_t ldh, double *T, int64_t ldt,
+                   double *Q, int64_t ldq, double *Z, int64_t ldz, cudaStream_t stream,
+                   ncclComm_t comm, const ht_opts *opts);
+int ht_stage2_z_ex(int64_t n, int64_t r, cuDoubleComplex *H, int64_t ldh, cuDoubleComplex *T,
+                   int64_t ldt, cuDoubleComplex *Q, int64_t ldq, cuDoubleComplex *Z,
+                   int64_t ldz, cudaStream_t stream, ncclComm_t comm, const ht_opts *opts);
+
+/* NCCL helpers: id_out receives NCCL_UNIQUE_ID_BYTES (128) bytes. */
+int ht_nccl_unique_id(void *id_out);
+int ht_comm_create(const void *id, int rank, int nranks, ncclComm_t *out);
+int ht_comm_destroy(ncclComm_t comm);
+
+/* Human-readable text for a return code (static storage). */
+const char *ht_strerror(int code);
+
+/* The paper's standard stage-two flop count ("10n^3 + O(n^2)"):
+ * 10 n^3 real, 40 n^3 real-equivalent for complex. */
+double ht_flops_std(int64_t n, int is_complex);
+
+/* Default q chosen for (n, r) when opts->q == 0 and HT_Q is unset. */
+int64_t ht_default_q(int64_t n, int64_t r, int is_complex);
+
+/* Instrumentation: per-kernel-class device time (ms) of the LAST call on this
+ * host thread: [0] chase (K1), [1] H/T right+left updates, [2] Q/Z updates,
+ * [3] whole call; and launches[0] = number of kernels launched by it. */
+int ht_last_timing(double *ms_out4, int64_t *launches_out);
+
+/* FP64 tensor-core (DMMA) peak probe: runs an mma.sync f64 loop on all SMs for
+ * `iters` iterations and returns the achieved TFLOP/s (device-timed). */
+double ht_probe_dmma_tflops(int iters);
+double ht_probe_dfma_tflops(int iters);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HT_STAGE2_H */
