@@ -1,0 +1,315 @@
+#!/usr/bin/env python
+"""Benchmark: stage-two HT reduction throughput on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl ours|reference]
+
+A step = one full ``ht_stage2`` call (all §8(a) rows: chase, accumulation, staircase,
+off-window and Q/Z updates) on the config's synthetic r-HT pencil, inputs restored from a
+pristine device copy inside the step (inputs 4 x n^2 x 8 B > 126 MB L2, so no L2 reuse across
+steps).  value = N x 10n^3 / t_step (the paper's standard count) in GFLOP/s;
+N > 1 runs N independent replicas (weak scaling; sharding is a later §8(e) row).
+
+--impl reference times the CPU oracle (Alg. 2, plain C, all host cores) on a bounded sample of
+the same workload (the leading n_s x n_s sub-pencil of the config's pencil, same r and
+generator) -- the only place besides cpu_baseline where bench.py executes oracle/.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from synth.pencil import CONFIGS, make_pencil  # noqa: E402
+
+METRIC = "stage-2 GFLOP/s and fraction of FP64 tensor roofline vs n, r at 1/2/4/8 B200"
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons DURING the timed region (B200_PROFILING.md)."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 7:
+                continue
+            try:
+                sm.append(float(p[0]))
+                mx.append(float(p[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, p[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_sample(cfg, n_s):
+    """Oracle (plain C Alg. 2, all host cores) on the leading n_s x n_s sub-pencil of config cfg."""
+    import oracle
+    c = CONFIGS[cfg]
+    H, T = make_pencil(c["n"] if c["n"] <= 4096 else n_s, c["r"], c["complex"], c["tdiag"], c["seed"])
+    H = np.asfortranarray(H[:n_s, :n_s])
+    T = np.asfortranarray(T[:n_s, :n_s])
+    cores = oracle.set_threads(len(os.sched_getaffinity(0)))
+    t0 = time.perf_counter()
+    oracle.stage2(H, T, c["r"])
+    dt = time.perf_counter() - t0
+    fl = (40.0 if c["complex"] else 10.0) * n_s ** 3
+    return fl / dt / 1e9, cores, dt
+
+
+def run_reference(args, rank):
+    if rank != 0:
+        return
+    c = CONFIGS[args.config]
+    n_s = args.sample_n or min(c["n"], 1536 if c["complex"] else 2048)
+    for _ in range(args.warmup):
+        cpu_sample(args.config, min(n_s, 512))
+    vals, times = [], []
+    cores = 1
+    for _ in range(args.steps):
+        v, cores, dt = cpu_sample(args.config, n_s)
+        vals.append(v)
+        times.append(dt)
+    v = statistics.mean(vals)
+    sample = (f"oracle (Alg. 2, plain C, OpenMP) full reduction of the leading {n_s}x{n_s} sub-pencil "
+              f"of config{args.config} (r={c['r']}, same generator/seed); rate = 10n_s^3/t")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "GFLOP/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.mean(times),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64" if not c["complex"] else "c128",
+        "data": "synthetic", "config": _config_dict(args, c, q=None),
+        "cpu_baseline": {"value": v, "unit": "GFLOP/s", "cores": cores, "kind": "oracle", "sample": sample},
+        "e2e": {"value": v, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def _config_dict(args, c, q):
+    d = {"workload": f"config{args.config}: n={c['n']} r={c['r']} {'complex' if c['complex'] else 'real'} fp64, "
+                     f"T diag {'graded 10^U(-3,0)' if c['tdiag'] == 'graded' else '1+|N(0,1)|'}, Q,Z accumulated",
+         "n": c["n"], "r": c["r"], "complex": c["complex"], "seed": c["seed"],
+         "l2": "inputs (4 n^2 fp64) larger than the 126 MB L2; restored from a device copy each step",
+         "parallelism": f"replicas x{args.gpus}"}
+    if q is not None:
+        d["q"] = q
+    return d
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--q", type=int, default=0)
+    ap.add_argument("--sample-n", type=int, default=0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+
+    import torch
+    import torch.distributed as dist
+    import paper_2301_07964_b200 as ht
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    c = CONFIGS[args.config]
+    n, r, cplx = c["n"], c["r"], c["complex"]
+    q = args.q or ht.default_q(n, r, cplx)
+    tdt = torch.complex128 if cplx else torch.float64
+
+    H_np, T_np = make_pencil(n, r, cplx, c["tdiag"], c["seed"])
+
+    def col_major_dev(A):
+        return torch.from_numpy(A).to(dev)  # Fortran-ordered numpy -> stride (1, n)
+
+    H0, T0 = col_major_dev(H_np), col_major_dev(T_np)
+    I0 = torch.eye(n, dtype=tdt, device=dev).t()
+    H, T = H0.clone(memory_format=torch.preserve_format), T0.clone(memory_format=torch.preserve_format)
+    Qd, Zd = I0.clone(memory_format=torch.preserve_format), I0.clone(memory_format=torch.preserve_format)
+    assert H.stride(0) == 1 and Qd.stride(0) == 1
+    stream = torch.cuda.current_stream(dev)
+
+    def step(profile=True):
+        H.copy_(H0)
+        T.copy_(T0)
+        Qd.copy_(I0)
+        Zd.copy_(I0)
+        ht.ht_stage2(H, T, r, Qd, Zd, stream=stream, q=q, profile=profile)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    clocks = ClockSampler(local)
+    barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    time.sleep(0.3)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    per = []
+    launches = 0
+    ev0.record(stream)
+    for _ in range(args.steps):
+        step()
+        ms, nl = ht.last_timing()
+        per.append(ms)
+        launches += nl
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    clk = clocks.stop()
+    ms_total = ev0.elapsed_time(ev1)
+    if world > 1:
+        t = torch.tensor([ms_total], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_total = float(t.item())
+    ms_step = ms_total / args.steps
+    fstd = ht.flops_std(n, cplx)
+    value = world * fstd / (ms_step * 1e-3) / 1e9
+    brk = {k: statistics.mean(p[k] for p in per) for k in per[0]}
+
+    # ---- roofline of the dominant kernel class (live CUDA-event durations) ----
+    peaks = _peaks()
+    dmma = ht.probe_dmma_tflops(20000)
+    fcnt_upd = (8.03 if not cplx else 8.03 * 4) * n ** 3  # counted update flops (H,T 4.03 + Q,Z 4.00) n^3
+    upd_ms = brk["ht_updates"] + brk["qz_updates"]
+    if brk["chase"] >= upd_ms:
+        # chase: latency-bound dependent chain of small FP64 reductions (reported against the FP64 ALU peak)
+        rq = (2.0 / 3.0) * r * r * n * n * (4 if cplx else 1)
+        band = 2.0 * r * (q + 2) * n * n * (4 if cplx else 1)
+        dfma = ht.probe_dfma_tflops(20000)
+        ach = (rq + band) / (brk["chase"] * 1e-3) / 1e12
+        roof = {"kernel": "chase_kernel (K1)", "bound": "alu", "achieved": ach, "peak": dfma, "unit": "TFLOP/s",
+                "frac": ach / dfma, "traffic": None,
+                "peak_source": "measured DFMA probe (ht_probe_dfma_tflops) on this GPU",
+                "algorithmic": "RQ (2/3)r^2n^2 + generate band 2r(q+2)n^2 flops per call"}
+    else:
+        ach = fcnt_upd / (upd_ms * 1e-3) / 1e12
+        roof = {"kernel": "row/col chain kernels (K3/K4)", "bound": "tensor", "achieved": ach, "peak": dmma,
+                "unit": "TFLOP/s", "frac": ach / dmma, "traffic": None,
+                "peak_source": "measured DMMA (mma.sync f64) probe on this GPU",
+                "algorithmic": "counted update flops 8.03n^3 per call"}
+    roof["share_of_step"] = max(brk["chase"], upd_ms) / ms_step
+
+    out = {
+        "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
+        "warmup": max(3, args.warmup), "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64" if not cplx else "c128", "data": "synthetic",
+        "config": _config_dict(args, c, q),
+        "roofline": roof,
+        "fraction_fp64_roofline": value / (world * dmma * 1e3),
+        "gflops_counted": world * (fcnt_upd) / (ms_step * 1e-3) / 1e9,
+        "breakdown_ms": brk, "dmma_peak_tflops": dmma,
+        "clocks": clk, "gpu_launches": launches,
+        "measured_peaks": {k: peaks.get(k) for k in ("hbm_gbs", "bf16_tflops")},
+    }
+
+    # ---- end to end: host pinned buffers -> device, C-ABI call, results -> host ----
+    if not args.no_e2e:
+        hp = [torch.from_numpy(A.T.copy()).pin_memory() for A in (H_np, T_np)]  # row-major of A^T
+        ip = torch.eye(n, dtype=tdt).pin_memory()
+        outs = [torch.empty((n, n), dtype=tdt).pin_memory() for _ in range(4)]
+        barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            H.t().copy_(hp[0], non_blocking=True)
+            T.t().copy_(hp[1], non_blocking=True)
+            Qd.t().copy_(ip, non_blocking=True)
+            Zd.t().copy_(ip, non_blocking=True)
+            ht.ht_stage2(H, T, r, Qd, Zd, stream=stream, q=q)
+            for o, X in zip(outs, (H, T, Qd, Zd)):
+                o.copy_(X.t(), non_blocking=True)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        e_ms = e0.elapsed_time(e1)
+        if world > 1:
+            t = torch.tensor([e_ms], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e_ms = float(t.item())
+        esz = 16 if cplx else 8
+        out["e2e"] = {"value": world * fstd / (e_ms / args.steps * 1e-3) / 1e9, "unit": "GFLOP/s",
+                      "h2d_bytes_per_step": 4 * n * n * esz, "d2h_bytes_per_step": 4 * n * n * esz}
+
+    if rank == 0 and not args.no_cpu:
+        n_s = args.sample_n or min(n, 1536 if cplx else 2048)
+        v, cores, dt = cpu_sample(args.config, n_s)
+        out["cpu_baseline"] = {
+            "value": v, "unit": "GFLOP/s", "cores": cores, "kind": "oracle",
+            "sample": f"oracle (Alg. 2, plain C, OpenMP) full reduction of the leading {n_s}x{n_s} sub-pencil of "
+                      f"config{args.config} (r={r}); {dt:.1f} s; rate = 10n_s^3/t"}
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -40,6 +40,7 @@
  *       or below T's diagonal) -- checked exactly on the device before work
  *    2  input has a non-finite entry (NaN/Inf) in H, T, Q or Z
  *    3  CUDA error   4  NCCL error   5  out of device memory
+ *    6  configuration not supported by this build (e.g. shared-memory limits)
  * No partial results are promised on error.
  *
  * Trivial cases: n <= 2 or r <= 1 is an exact no-op.  r >= n-1 is allowed.
@@ -63,7 +64,8 @@ extern "C" {
 /* Tunables (NULL = defaults).  q: sweeps per group ("q");
  * 0 = default (environment HT_Q, else a per-r choice documented in DESIGN.md).
  * chase_ctas: CTAs of the wavefront chase kernel (0 = min(q, 32)).
- * root: result rank for comm != NULL.  flags: bit 0 = skip input validation. */
+ * root: result rank for comm != NULL.  flags: bit 0 = skip input validation,
+ * bit 1 = record per-kernel-class device times (see ht_last_timing). */
 typedef struct ht_opts {
     int64_t q;
     int32_t chase_ctas;
@@ -73,6 +75,7 @@ typedef struct ht_opts {
 } ht_opts;
 
 #define HT_FLAG_NO_VALIDATE 1
+#define HT_FLAG_PROFILE 2 /* record per-kernel-class device times (ht_last_timing) */
 
 /* Real FP64 stage two.  Arguments 1..12 in order: n, r, H, ldh, T, ldt,
  * Q, ldq, Z, ldz, stream, comm. */

@@ -95,7 +95,7 @@ def default_q(n: int, r: int, is_complex: bool = False) -> int:
 
 
 def last_timing():
-    """(ms dict, launches) of the last call on this thread (timings need HT_PROFILE=1)."""
+    """(ms dict, launches) of the last call on this thread (timings need profile=True)."""
     ms = (ctypes.c_double * 4)()
     nl = ctypes.c_int64()
     _load().ht_last_timing(ms, ctypes.byref(nl))
@@ -124,7 +124,7 @@ def _check_mat(X, n, name, dtype):
 
 
 def ht_stage2(H, T, r: int, Q=None, Z=None, stream=None, q: int = 0, chase_ctas: int = 0,
-              validate: bool = True, comm=None):
+              validate: bool = True, profile: bool = False, comm=None):
     """In-place stage two on device tensors (C ABI ``ht_stage2_{d,z}_ex``).
 
     H, T: n x n column-major CUDA tensors (float64 or complex128) holding an r-HT pencil.
@@ -142,7 +142,8 @@ def ht_stage2(H, T, r: int, Q=None, Z=None, stream=None, q: int = 0, chase_ctas:
     pq, ldq = _check_mat(Q, n, "Q", dt)
     pz, ldz = _check_mat(Z, n, "Z", dt)
     s = stream if stream is not None else torch.cuda.current_stream(H.device)
-    opts = Opts(q=int(q), chase_ctas=int(chase_ctas), root=0, flags=0 if validate else 1)
+    opts = Opts(q=int(q), chase_ctas=int(chase_ctas), root=0,
+                flags=(0 if validate else 1) | (2 if profile else 0))
     fn = lib.ht_stage2_z_ex if cplx else lib.ht_stage2_d_ex
     rc = fn(n, int(r), ph, ldh, pt, ldt, pq, ldq, pz, ldz, ctypes.c_void_p(s.cuda_stream),
             ctypes.c_void_p(comm) if comm else None, ctypes.byref(opts))

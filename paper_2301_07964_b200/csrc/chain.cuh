@@ -1,209 +1,391 @@
 // chain.cuh -- K3/K4: the apply phase of one group (Alg. 4
-// "Application phase of stage two", corrected per DESIGN.md §3 / c8), as fused
-// descending-k chains:
+// "Application phase of stage two", corrected per DESIGN.md §3 / c8) as fused
+// descending-k GEMM chains on the FP64 tensor cores (mma.sync f64 -> DMMA.8x8x4).
 //
-//   row chain  (right updates, row-independent):  M(rows, C_k) <- M(rows, C_k) X_k,
-//              k = K-1 ... 0, X_k = V_k (A, B, Z) or U_k (Q).  One CTA owns a tile of
-//              BM rows and streams the windows right-to-left, keeping the q-1 overlap
-//              columns of consecutive windows on chip (each entry read/written once per
-//              group).  For A and B the tile rows split per window into the dense block
-//              region (rows <= i5), the staircase (rows i5s..i4, reflector by reflector,
-//              Alg. 4 lines 4-9), and untouched rows.
-//   col chain  (left updates, column-independent): M(R_k, cols) <- U_k^* M(R_k, cols)
-//              for columns > i5 (A) / > i6 (B), Alg. 4 lines 16-25.
-//
-// Windows: C_k = R_k = [j1+kr+1, min(j1+q-1+(k+1)r, n)], width wk <= w = q+r-1.
+// One CTA owns a tile of BM "tile rows" of one matrix and streams the group's windows
+// k = kstart ... kend (descending):
+//   non-transposed (right updates  M(rows, C_k) <- M(rows, C_k) X_k):  tile rows = matrix
+//       rows, chain index = matrix columns; X_k = V_k (H, T, Z) or U_k (Q);
+//   transposed (left updates  M(R_k, cols) <- U_k^* M(R_k, cols)): tile rows = matrix
+//       columns, chain index = matrix rows; computed as M^T <- M^T conj(U_k).
+// The tile's window columns live in a circular on-chip buffer of w+r columns: window k
+// occupies [p_k, p_k+w_k), window k-1 starts r columns earlier, so the q-1 overlap columns
+// stay in place between windows (each entry of M is read and written once per group), the
+// r fresh columns of the next window are prefetched (cp.async) while the current window
+// computes, and the w x w blocks stream through a 3-stage ring filled by bulk async copies
+// (cp.async.bulk + mbarrier, SASS UBLKCP).
+// Rows of H/T right updates split per window into the block region (rows <= i5), the
+// staircase (rows i5s..i4(k,j), reflector by reflector, Alg. 4 lines 4-9) and untouched
+// rows; left updates touch columns > i5 (H) / > i6 (T) only.
 #pragma once
 #include "scalar.cuh"
-#include "chase.cuh"
+
+#ifndef IDX
+#define IDX(p, ld, i, j) (p)[((int64_t)(i) - 1) + ((int64_t)(j) - 1) * (int64_t)(ld)]
+#endif
+
+enum ChainMode { CM_PLAIN = 0, CM_AB_RIGHT = 1, CM_A_LEFT = 2, CM_B_LEFT = 3 };
 
 template <typename S>
-struct ChainArgs {
-    int n, r, qp, j1, K, W;
-    S* M0;
-    int64_t ld0;
-    S* M1;
-    int64_t ld1;
-    const S* Blk0;  // blocks for M0 (U or V)
-    const S* Blk1;  // blocks for M1
-    const S* Zr;    // staircase reflectors (row chain on A/B)
-    int kcnt_base;  // unused (reserved)
+struct ChainJob {
+    S* M;
+    int64_t ld;
+    const S* Blk;  // K blocks, each WP rows x LDB (row-major, padded rows/cols zero)
+    int mode;
+    int trans;
+    int ntiles;
 };
 
-__device__ __forceinline__ int imax(int a, int b) { return a > b ? a : b; }
+template <typename S>
+struct ChainParams {
+    int n, r, qp, j1, K;
+    ChainJob<S> job[2];
+    int njobs;
+    const S* Zr;  // staircase reflectors: (qp*K) records of (r+1)
+};
 
-// ---------------------------------------------------------------------------------------
-// Row chain.  AB = true: A/B right updates (masks + staircase).  AB = false: Q or Z.
-// grid.x = row tiles, grid.y = matrix (0 -> M0/Blk0, 1 -> M1/Blk1).
-// smem: X [BM x W] (column slot = global col mod W, ld BM), Y [BM x W], Vs [W x W].
-template <typename S, int BM, int NT, bool AB>
-__global__ void __launch_bounds__(NT) row_chain_kernel(ChainArgs<S> a) {
-    extern __shared__ __align__(16) unsigned char smraw[];
-    S* X = reinterpret_cast<S*>(smraw);
-    const int W = a.W;
-    S* Y = X + (size_t)BM * W;
-    S* Vs = Y + (size_t)BM * W;
-    const int n = a.n, r = a.r, qp = a.qp, j1 = a.j1, K = a.K;
-    const int w = qp + r - 1;
-    S* M = blockIdx.y == 0 ? a.M0 : a.M1;
-    const int64_t ld = blockIdx.y == 0 ? a.ld0 : a.ld1;
-    const S* Blk = blockIdx.y == 0 ? a.Blk0 : a.Blk1;
-    const int R0 = blockIdx.x * BM + 1;
-    if (R0 > n) return;
-    const int nr = min(BM, n - R0 + 1);
-    const int tid = threadIdx.x;
-    // rows touched by window k in the apply phase (A/B): block rows <= i5b(k), staircase
-    // rows <= max_t i4(k,t) = j1 + k r (q >= 2)
-    auto rowmax = [&](int k) {
-        return (qp >= 2) ? j1 + imax(0, k * r) : j1 + imax(0, (k - qp + 1) * r);
-    };
-    if (AB && rowmax(K - 1) < R0) return;
-    int pc0 = 0, pwk = 0;
-    for (int k = K - 1; k >= 0; --k) {
-        if (AB && rowmax(k) < R0) break;
-        const int c0 = j1 + k * r + 1;
-        const int wk = min(w, n - c0 + 1);
-        // write out columns leaving the window, then load the entering ones
-        if (pwk > 0) {
-            for (int e = tid; e < nr * (pc0 + pwk - (c0 + wk)); e += NT) {
-                const int i = e % nr, c = c0 + wk + e / nr;
-                IDX(M, ld, R0 + i, c) = X[i + (c % W) * BM];
-            }
-            __syncthreads();
-        }
-        const int cin1 = (pwk > 0) ? pc0 : c0 + wk;  // entering columns [c0, cin1)
-        for (int e = tid; e < nr * (cin1 - c0); e += NT) {
-            const int i = e % nr, c = c0 + e / nr;
-            X[i + (c % W) * BM] = IDX(M, ld, R0 + i, c);
-        }
-        const S* Bk = Blk + (int64_t)k * W * W;
-        for (int e = tid; e < wk * wk; e += NT) {
-            const int l = e % wk, c = e / wk;
-            Vs[l + c * W] = Bk[l + (int64_t)c * W];
-        }
-        __syncthreads();
-        // Y = X(:, window) * Vs
-        const int i5b = j1 + imax(0, (k - qp + 1) * r);
-        for (int e = tid; e < nr * wk; e += NT) {
-            const int i = e % nr, c = e / nr;
-            S acc = S(0.0);
-            for (int l = 0; l < wk; ++l) acc = fma_s(X[i + ((c0 + l) % W) * BM], Vs[l + c * W], acc);
-            Y[i + c * BM] = acc;
-        }
-        __syncthreads();
-        for (int e = tid; e < nr * wk; e += NT) {
-            const int i = e % nr, c = e / nr;
-            if (!AB || R0 + i <= i5b) X[i + ((c0 + c) % W) * BM] = Y[i + c * BM];
-        }
-        __syncthreads();
-        if (AB) {  // staircase (Alg. 4 lines 4-9, corrected): rows i5s..i4(k,j), j = j1+1..j1+q-1
-            const int i5s = j1 + 1 + imax(0, (k - qp + 1) * r);
-            const int rlo = imax(i5s, R0), rhi = min(rowmax(k), R0 + nr - 1);
-            if (rlo <= rhi) {
-                for (int i = tid; i < nr; i += NT) {  // one thread per row: sequential in t
-                    const int row = R0 + i;
-                    if (row < rlo || row > rhi) continue;
-                    for (int t = 1; t < qp; ++t) {
-                        const int j = j1 + t;
-                        const int i1 = j + k * r + 1, i2 = min(j + (k + 1) * r, n);
-                        const int m = i2 - i1 + 1;
-                        if (m < 2) continue;
-                        const int i4a = j1 + imax(0, (k + t - qp + 1) * r);
-                        if (row > i4a) continue;
-                        const S* zr = a.Zr + ((int64_t)t * K + k) * (r + 1);
-                        const S sig = zr[r];
-                        if (is_zero(sig)) continue;
-                        S s = S(0.0);
-                        for (int c = 0; c < m; ++c) s = fma_s(X[i + ((i1 + c) % W) * BM], zr[c], s);
-                        s = s * sig;
-                        for (int c = 0; c < m; ++c) X[i + ((i1 + c) % W) * BM] -= s * conjv(zr[c]);
-                    }
-                }
-                __syncthreads();
-            }
-        }
-        pc0 = c0;
-        pwk = wk;
-    }
-    if (pwk > 0) {
-        for (int e = tid; e < nr * pwk; e += NT) {
-            const int i = e % nr, c = pc0 + e / nr;
-            IDX(M, ld, R0 + i, c) = X[i + (c % W) * BM];
-        }
-    }
+constexpr int CH_BM = 64;      // tile rows per CTA
+constexpr int CH_NT = 256;     // 8 warps: 2 (rows) x 4 (cols)
+constexpr int CH_KC = 16;      // k rows per ring chunk
+constexpr int CH_STAGES = 3;   // ring depth
+constexpr int CH_LDX = CH_BM + 8;  // smem column stride of X (== 8 mod 16: conflict-free)
+
+__host__ __device__ constexpr int chain_ldb(int WP) { return WP + 8; }
+
+// dynamic smem: [64 B mbarriers][circular X: (w+r) x CH_LDX][block ring][staircase refl.]
+template <typename S, int WP>
+__host__ __device__ constexpr size_t chain_smem_bytes(int r, int q) {
+    return 64 + (size_t)(q + r - 1 + r) * CH_LDX * sizeof(S) +
+           (size_t)CH_STAGES * CH_KC * chain_ldb(WP) * sizeof(S) + (size_t)(q + 1) * (r + 1) * sizeof(S);
+}
+
+// ---- PTX helpers ---------------------------------------------------------------------
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void cp_async8(void* s, const void* g) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(s)), "l"(g));
+}
+__device__ __forceinline__ void cp_async16(void* s, const void* g) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(s)), "l"(g));
+}
+template <typename S>
+__device__ __forceinline__ void cp_async_elem(S* s, const S* g) {
+    if constexpr (sizeof(S) == 8) cp_async8(s, g);
+    else cp_async16(s, g);
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* s, const void* g, unsigned bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+            smem_u32(s)),
+        "l"(g), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+        : "+d"(c0), "+d"(c1)
+        : "d"(a), "d"(b));
+}
+
+template <typename S>
+struct Acc;
+template <>
+struct Acc<double> {
+    double v[2];
+};
+template <>
+struct Acc<zc> {
+    double re[2], im[2];
+};
+
+// One k-step of 4 on an 8x8 tile: acc += a (8x4) * b (4x8); complex = 4 real DMMAs.
+__device__ __forceinline__ void mma_step(Acc<double>& c, double a, double b) { dmma(c.v[0], c.v[1], a, b); }
+__device__ __forceinline__ void mma_step(Acc<zc>& c, zc a, zc b) {
+    dmma(c.re[0], c.re[1], a.x, b.x);
+    dmma(c.re[0], c.re[1], -a.y, b.y);
+    dmma(c.im[0], c.im[1], a.x, b.y);
+    dmma(c.im[0], c.im[1], a.y, b.x);
+}
+__device__ __forceinline__ double acc_get(const Acc<double>& c, int h) { return c.v[h]; }
+__device__ __forceinline__ zc acc_get(const Acc<zc>& c, int h) { return zc(c.re[h], c.im[h]); }
+__device__ __forceinline__ void acc_zero(Acc<double>& c) { c.v[0] = c.v[1] = 0.0; }
+__device__ __forceinline__ void acc_zero(Acc<zc>& c) { c.re[0] = c.re[1] = c.im[0] = c.im[1] = 0.0; }
+
+template <typename S>
+__device__ __forceinline__ S maybe_conj(S x, bool c) {
+    if constexpr (sizeof(S) == 8) return x;
+    else return c ? conjv(x) : x;
 }
 
 // ---------------------------------------------------------------------------------------
-// Column chain (left updates of A (M0, cols > i5) and B (M1, cols > i6)).
-// grid.x = column tiles of BN, grid.y = matrix.  smem: X [W x BN] (row slot = row mod W,
-// ld W+1), Y [W x BN], Us [W x W].
-template <typename S, int BN, int NT>
-__global__ void __launch_bounds__(NT) col_chain_kernel(ChainArgs<S> a) {
+template <typename S, int WP>
+__global__ void __launch_bounds__(CH_NT) chain_kernel(ChainParams<S> P) {
     extern __shared__ __align__(16) unsigned char smraw[];
-    const int W = a.W;
-    const int LDX = W + 1;
-    S* X = reinterpret_cast<S*>(smraw);
-    S* Y = X + (size_t)LDX * BN;
-    S* Us = Y + (size_t)LDX * BN;
-    const int n = a.n, r = a.r, qp = a.qp, j1 = a.j1, K = a.K;
+    constexpr int LDB = chain_ldb(WP);
+    constexpr int MT = 4;            // 8-row tiles per warp (32 rows)
+    constexpr int NTL = WP / 32;     // 8-col tiles per warp (WP/4 cols)
+    const int n = P.n, r = P.r, qp = P.qp, j1 = P.j1, K = P.K;
     const int w = qp + r - 1;
-    const bool isA = blockIdx.y == 0;
-    S* M = isA ? a.M0 : a.M1;
-    const int64_t ld = isA ? a.ld0 : a.ld1;
-    const S* Blk = a.Blk0;
-    const int C0 = blockIdx.x * BN + 1;
-    if (C0 > n) return;
-    const int nc = min(BN, n - C0 + 1);
-    const int C1 = C0 + nc - 1;
-    const int tid = threadIdx.x;
-    auto cstart = [&](int k) {  // columns > cstart(k) receive U_k^*  (corrected i5 / i6)
-        return isA ? j1 + qp - 1 + imax(0, (k - 1) * r + 1) : j1 + qp + (k + 1) * r - 1;
+    const int CIRC = w + r;  // circular buffer columns
+
+    // ---- which job / tile ----
+    int bid = blockIdx.x, jb_ = 0;
+    if (P.njobs > 1 && bid >= P.job[0].ntiles) {
+        bid -= P.job[0].ntiles;
+        jb_ = 1;
+    }
+    const ChainJob<S> J = P.job[jb_];
+    const int mode = J.mode;
+    const bool trans = J.trans != 0;
+    const int R0 = bid * CH_BM + 1;  // first tile row (1-based)
+    if (R0 > n) return;
+    const int nr = min(CH_BM, n - R0 + 1);
+    const int R1 = R0 + nr - 1;
+
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smraw);
+    S* X = reinterpret_cast<S*>(smraw + 64);
+    S* ring = X + (size_t)CIRC * CH_LDX;
+    S* zsm = ring + (size_t)CH_STAGES * CH_KC * LDB;
+
+    // ---- window range of this tile ----
+    auto rowmax = [&](int k) {  // last row touched by window k in the apply phase (H, T right)
+        return (qp >= 2) ? j1 + max(0, k * r) : j1 + max(0, (k - qp + 1) * r);
     };
-    int kmax = K - 1;
-    while (kmax >= 0 && cstart(kmax) >= C1) --kmax;
-    if (kmax < 0) return;
-    int pc0 = 0, pwk = 0;
-    for (int k = kmax; k >= 0; --k) {
+    auto cstart = [&](int k) {  // left updates touch columns > cstart(k) (corrected i5 / i6)
+        return mode == CM_A_LEFT ? j1 + qp - 1 + max(0, (k - 1) * r + 1) : j1 + qp + (k + 1) * r - 1;
+    };
+    int kstart = K - 1, kend = 0;
+    if (mode == CM_AB_RIGHT) {
+        if (rowmax(K - 1) < R0) return;
+        while (kend < K - 1 && rowmax(kend) < R0) ++kend;
+    } else if (mode == CM_A_LEFT || mode == CM_B_LEFT) {
+        while (kstart >= 0 && cstart(kstart) >= R1) --kstart;
+        if (kstart < 0) return;
+    }
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wm = warp & 1, wn = warp >> 1;
+
+    // zero the circular buffer (padded K rows of the blocks are zero; keep X finite)
+    for (int e = tid; e < CIRC * CH_LDX; e += CH_NT) X[e] = S(0.0);
+    if (tid == 0) {
+        for (int s = 0; s < CH_STAGES; ++s) mbar_init(&bars[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+
+    // global element access (1-based tile row g, chain index c)
+    auto gptr = [&](int g, int c) -> S* {
+        return trans ? &IDX(J.M, J.ld, c, g) : &IDX(J.M, J.ld, g, c);
+    };
+    // load chain indices [c0, c0+cnt) into circular positions starting at p (cp.async)
+    auto load_cols = [&](int c0, int cnt, int p) {
+        if (!trans) {
+            for (int e = tid; e < cnt * nr; e += CH_NT) {
+                const int i = e % nr, l = e / nr;
+                int pos = p + l;
+                if (pos >= CIRC) pos -= CIRC;
+                cp_async_elem(&X[pos * CH_LDX + i], gptr(R0 + i, c0 + l));
+            }
+        } else {
+            for (int e = tid; e < cnt * nr; e += CH_NT) {
+                const int l = e % cnt, i = e / cnt;
+                int pos = p + l;
+                if (pos >= CIRC) pos -= CIRC;
+                cp_async_elem(&X[pos * CH_LDX + i], gptr(R0 + i, c0 + l));
+            }
+        }
+    };
+    auto store_cols = [&](int c0, int cnt, int p) {
+        if (!trans) {
+            for (int e = tid; e < cnt * nr; e += CH_NT) {
+                const int i = e % nr, l = e / nr;
+                int pos = p + l;
+                if (pos >= CIRC) pos -= CIRC;
+                *gptr(R0 + i, c0 + l) = X[pos * CH_LDX + i];
+            }
+        } else {
+            for (int e = tid; e < cnt * nr; e += CH_NT) {
+                const int l = e % cnt, i = e / cnt;
+                int pos = p + l;
+                if (pos >= CIRC) pos -= CIRC;
+                *gptr(R0 + i, c0 + l) = X[pos * CH_LDX + i];
+            }
+        }
+    };
+
+    // ---- block ring producer (thread 0): chunk sequence over (window, chunk) ----
+    int pk = kstart, pc = 0;  // next chunk to issue
+    unsigned pseq = 0;
+    auto nchunks = [&](int k) {
+        const int wk = min(w, n - (j1 + k * r + 1) + 1);
+        return (wk + CH_KC - 1) / CH_KC;
+    };
+    auto issue_next = [&]() {
+        if (tid != 0 || pk < kend) return;
+        const int s = pseq % CH_STAGES;
+        const S* src = J.Blk + ((size_t)pk * WP + (size_t)pc * CH_KC) * LDB;
+        mbar_expect_tx(&bars[s], CH_KC * LDB * sizeof(S));
+        bulk_g2s(ring + (size_t)s * CH_KC * LDB, src, CH_KC * LDB * sizeof(S), &bars[s]);
+        ++pseq;
+        if (++pc == nchunks(pk)) {
+            pc = 0;
+            --pk;
+        }
+    };
+    for (int s = 0; s < CH_STAGES - 1; ++s) issue_next();
+
+    // first window: all of its columns
+    int p = 0;  // circular position of the current window's first column
+    {
+        const int c0 = j1 + kstart * r + 1;
+        load_cols(c0, min(w, n - c0 + 1), 0);
+        cp_async_commit();
+    }
+    unsigned cseq = 0;  // consumer chunk sequence
+    for (int k = kstart; k >= kend; --k) {
         const int c0 = j1 + k * r + 1;
         const int wk = min(w, n - c0 + 1);
-        if (pwk > 0) {
-            const int nl = pc0 + pwk - (c0 + wk);
-            for (int e = tid; e < nl * nc; e += NT) {
-                const int i = c0 + wk + e % nl, c = e / nl;
-                IDX(M, ld, i, C0 + c) = X[(i % W) + c * LDX];
+        const bool has_next = k - 1 >= kend;
+        const int cn = has_next ? min(qp - 1, wk) : 0;  // carried into window k-1
+        cp_async_wait_all();
+        __syncthreads();
+        // prefetch: fresh columns of window k-1 and (H/T right) window k's staircase reflectors
+        if (has_next) {
+            int pn = p - r;
+            if (pn < 0) pn += CIRC;
+            load_cols(c0 - r, r, pn);
+        }
+        const int i5s = j1 + 1 + max(0, (k - qp + 1) * r);
+        const bool stair = mode == CM_AB_RIGHT && qp >= 2 && max(i5s, R0) <= min(rowmax(k), R1);
+        if (stair) {
+            const S* src = P.Zr + (size_t)k * (r + 1);
+            for (int e = tid; e < (qp - 1) * (r + 1); e += CH_NT) {
+                const int t = 1 + e / (r + 1), c = e % (r + 1);
+                cp_async_elem(&zsm[(size_t)t * (r + 1) + c], src + (size_t)t * K * (r + 1) + c);
             }
+        }
+        cp_async_commit();
+
+        // ---- Y = X(:, window) * B_k on the tensor cores ----
+        Acc<S> acc[MT][NTL];
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+            for (int nt = 0; nt < NTL; ++nt) acc_zero(acc[mt][nt]);
+        const int nch = (wk + CH_KC - 1) / CH_KC;
+        const int rowb = wm * 32 + (lane >> 2);
+        const int colb = wn * (WP / 4) + (lane >> 2);
+        for (int ch = 0; ch < nch; ++ch) {
+            const int s = cseq % CH_STAGES;
+            mbar_wait(&bars[s], (cseq / CH_STAGES) & 1);
+            __syncthreads();  // everyone is past chunk cseq-1: its stage may be refilled
+            issue_next();
+            const S* Bs = ring + (size_t)s * CH_KC * LDB;
+#pragma unroll
+            for (int kk = 0; kk < CH_KC; kk += 4) {
+                const int kl = ch * CH_KC + kk + (lane & 3);  // window-local column (K index)
+                int pos = p + kl;
+                if (pos >= CIRC) pos -= CIRC;
+                if (pos >= CIRC) pos -= CIRC;
+                S a[MT], b[NTL];
+#pragma unroll
+                for (int mt = 0; mt < MT; ++mt) a[mt] = X[pos * CH_LDX + rowb + mt * 8];
+#pragma unroll
+                for (int nt = 0; nt < NTL; ++nt)
+                    b[nt] = maybe_conj(Bs[(kk + (lane & 3)) * LDB + colb + nt * 8], trans);
+#pragma unroll
+                for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+                    for (int nt = 0; nt < NTL; ++nt) mma_step(acc[mt][nt], a[mt], b[nt]);
+            }
+            ++cseq;
+        }
+        __syncthreads();  // all reads of X done
+        // ---- epilogue: write Y back in place for the rows the mode updates ----
+        const int ylo = (mode == CM_A_LEFT || mode == CM_B_LEFT) ? cstart(k) : 0;
+        const int yhi = (mode == CM_AB_RIGHT) ? j1 + max(0, (k - qp + 1) * r) : 0x7fffffff;
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) {
+            const int row = rowb + mt * 8;
+            const int g = R0 + row;
+            const bool upd = row < nr && g > ylo && g <= yhi;
+#pragma unroll
+            for (int nt = 0; nt < NTL; ++nt)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int col = wn * (WP / 4) + nt * 8 + (lane & 3) * 2 + h;
+                    if (upd && col < wk) {
+                        int pos = p + col;
+                        if (pos >= CIRC) pos -= CIRC;
+                        X[pos * CH_LDX + row] = maybe_conj(acc_get(acc[mt][nt], h), false);
+                    }
+                }
+        }
+        if (stair) {  // Alg. 4 lines 4-9: rows i5s..i4(k,j) get Z_k^j one by one, j ascending
+            cp_async_wait_all();
             __syncthreads();
-        }
-        const int rin1 = (pwk > 0) ? pc0 : c0 + wk;
-        const int ne = rin1 - c0;
-        for (int e = tid; e < ne * nc; e += NT) {
-            const int i = c0 + e % ne, c = e / ne;
-            X[(i % W) + c * LDX] = IDX(M, ld, i, C0 + c);
-        }
-        const S* Bk = Blk + (int64_t)k * W * W;
-        for (int e = tid; e < wk * wk; e += NT) {
-            const int l = e % wk, c = e / wk;
-            Us[l + c * W] = Bk[l + (int64_t)c * W];
+            const int row = tid >> 2, part = tid & 3;  // 4 threads per row
+            const int g = R0 + row;
+            const bool active = row < nr && g >= i5s && g <= rowmax(k);
+            for (int t = 1; t < qp; ++t) {
+                const int j = j1 + t;
+                const int i1 = j + k * r + 1, i2 = min(j + (k + 1) * r, n);
+                const int m = i2 - i1 + 1;
+                if (m < 2 || k >= min(K, 2 + (n - j - 1) / r)) continue;
+                const int i4a = j1 + max(0, (k + t - qp + 1) * r);
+                const S* zr = zsm + (size_t)t * (r + 1);
+                const S sig = zr[r];
+                if (is_zero(sig)) continue;
+                S sdot = S(0.0);
+                if (active && g <= i4a)
+                    for (int c = part; c < m; c += 4) {
+                        int pos = p + t + c;
+                        if (pos >= CIRC) pos -= CIRC;
+                        sdot = fma_s(X[pos * CH_LDX + row], zr[c], sdot);
+                    }
+                sdot += shfl_xor(sdot, 1);
+                sdot += shfl_xor(sdot, 2);
+                if (active && g <= i4a) {
+                    sdot = sdot * sig;
+                    for (int c = part; c < m; c += 4) {
+                        int pos = p + t + c;
+                        if (pos >= CIRC) pos -= CIRC;
+                        X[pos * CH_LDX + row] -= sdot * conjv(zr[c]);
+                    }
+                }
+            }
         }
         __syncthreads();
-        const int cs = cstart(k);
-        for (int e = tid; e < nc * wk; e += NT) {
-            const int c = e % nc, i = e / nc;
-            S acc = S(0.0);
-            for (int l = 0; l < wk; ++l) acc += conj_mul(Us[l + i * W], X[((c0 + l) % W) + c * LDX]);
-            Y[i + c * LDX] = acc;
+        // columns [cn, wk) are final for this group; [0, cn) stay as window k-1's carry
+        {
+            int po = p + cn;
+            if (po >= CIRC) po -= CIRC;
+            store_cols(c0 + cn, wk - cn, po);
         }
-        __syncthreads();
-        for (int e = tid; e < nc * wk; e += NT) {
-            const int c = e % nc, i = e / nc;
-            if (C0 + c > cs) X[((c0 + i) % W) + c * LDX] = Y[i + c * LDX];
-        }
-        __syncthreads();
-        pc0 = c0;
-        pwk = wk;
+        p -= r;
+        if (p < 0) p += CIRC;
     }
-    for (int e = tid; e < pwk * nc; e += NT) {
-        const int i = pc0 + e % pwk, c = e / pwk;
-        IDX(M, ld, i, C0 + c) = X[(i % W) + c * LDX];
-    }
+    cp_async_wait_all();
 }

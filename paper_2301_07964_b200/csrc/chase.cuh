@@ -20,13 +20,13 @@
 
 template <typename S>
 struct ChaseArgs {
-    int n, r, qp, j1, K, W;
+    int n, r, qp, j1, K, WP, LDB;
     S* A;
     int64_t lda;
     S* B;
     int64_t ldb;
-    S* U;     // K dense blocks, W x W column-major (window k at U + k*W*W)
-    S* V;
+    S* U;     // K dense blocks, row-major: (l, c) at U[k*WP*LDB + l*LDB + c]
+    S* V;     // (rows/cols >= w_k are zero; U_k, V_k start as I_{w_k})
     S* Zr;    // (qp*K) records of (r+1): Z_k^j vector (m entries), sigma at [r]
     int* prog;  // qp counters: steps completed by each sweep of the group
 };
@@ -74,7 +74,7 @@ template <typename S, int NT>
 __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
     extern __shared__ __align__(16) unsigned char smraw[];
     S* sm = reinterpret_cast<S*>(smraw);
-    const int n = a.n, r = a.r, qp = a.qp, j1 = a.j1, K = a.K, W = a.W;
+    const int n = a.n, r = a.r, qp = a.qp, j1 = a.j1, K = a.K, LDB = a.LDB;
     const int w = qp + r - 1;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     constexpr int NW = NT / 32;
@@ -111,8 +111,8 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
             const int b0 = j1 + k * r + 1;
             const int m = i2 - i1 + 1;
             const int wk = min(w, n - b0 + 1);
-            S* Uk = a.U + (int64_t)k * W * W;
-            S* Vk = a.V + (int64_t)k * W * W;
+            S* Uk = a.U + (int64_t)k * a.WP * LDB;
+            S* Vk = a.V + (int64_t)k * a.WP * LDB;
             const int L = (t > 0) ? min(j - 1 + (k + 1) * r, n) - b0 + 1 : 0;
             const int nx = i2 - b0 + 1;
             const int cB = i1 + r - 1;  // == i2 when it exists
@@ -125,10 +125,9 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
                 __syncthreads();
                 if (L >= 1) {
                     for (int o = warp; o < L; o += NW) {
-                        const S* Ucol = Uk + (int64_t)o * W;
                         S s = S(0.0), s2 = S(0.0);
                         for (int l = lane; l < L; l += 32) {
-                            const S u = ldcg(&Ucol[l]);
+                            const S u = ldcg(&Uk[(int64_t)l * LDB + o]);
                             s += conj_mul(u, xs[l]);
                             if (hasB) s2 += conj_mul(u, ys[l]);
                         }
@@ -186,10 +185,10 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
                         }
                         for (int l = tid; l < wk; l += NT) {  // U_k <- U_k Q_k^j
                             S s = S(0.0);
-                            for (int c = 0; c < m; ++c) s += ldcg(&Uk[l + (int64_t)(t + c) * W]) * vq[c];
+                            for (int c = 0; c < m; ++c) s += ldcg(&Uk[(int64_t)l * LDB + t + c]) * vq[c];
                             s = s * tau;
                             for (int c = 0; c < m; ++c) {
-                                S* p = &Uk[l + (int64_t)(t + c) * W];
+                                S* p = &Uk[(int64_t)l * LDB + t + c];
                                 *p = ldcg(p) - s * conjv(vq[c]);
                             }
                         }
@@ -280,10 +279,10 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
                     if (!is_zero(sig)) {
                         for (int l = tid; l < wk; l += NT) {  // V_k <- V_k Z_k^j
                             S s = S(0.0);
-                            for (int c = 0; c < m; ++c) s += ldcg(&Vk[l + (int64_t)(t + c) * W]) * vz[c];
+                            for (int c = 0; c < m; ++c) s += ldcg(&Vk[(int64_t)l * LDB + t + c]) * vz[c];
                             s = s * sig;
                             for (int c = 0; c < m; ++c) {
-                                S* p = &Vk[l + (int64_t)(t + c) * W];
+                                S* p = &Vk[(int64_t)l * LDB + t + c];
                                 *p = ldcg(p) - s * conjv(vz[c]);
                             }
                         }

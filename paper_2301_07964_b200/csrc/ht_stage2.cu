@@ -9,10 +9,11 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <vector>
 
 #include "../../include/ht_stage2.h"
-#include "chain.cuh"
 #include "chase.cuh"
+#include "chain.cuh"
 #include "misc.cuh"
 #include "scalar.cuh"
 
@@ -25,16 +26,7 @@ thread_local double g_last_ms[4] = {0, 0, 0, 0};
 thread_local int64_t g_last_launches = 0;
 
 constexpr int CHASE_NT = 256;
-constexpr int CHAIN_NT = 256;
-constexpr int ROW_BM = 64;
-constexpr int COL_BN = 64;
 
-struct Timer {
-    bool on = false;
-    cudaStream_t s = nullptr;
-    cudaEvent_t ev[2] = {nullptr, nullptr};
-    float acc = 0;
-};
 
 #define CK(x)                                                                     \
     do {                                                                          \
@@ -56,22 +48,44 @@ int64_t default_q(int64_t n, int64_t r, int is_complex) {
     return std::max<int64_t>(1, std::min<int64_t>(q, std::max<int64_t>(1, n - 2)));
 }
 
-template <typename S>
-size_t row_chain_smem(int W) { return ((size_t)2 * ROW_BM * W + (size_t)W * W) * sizeof(S); }
-template <typename S>
-size_t col_chain_smem(int W) { return ((size_t)2 * (W + 1) * COL_BN + (size_t)W * W) * sizeof(S); }
+template <typename S, int WP>
+size_t chain_bytes(int r, int q) { return chain_smem_bytes<S, WP>(r, q); }
+
+template <typename S, int WP>
+int launch_chain(const ChainParams<S>& P, int grid, int r, int q, cudaStream_t st) {
+    const size_t bytes = chain_bytes<S, WP>(r, q);
+    static bool attr_set = false;  // per instantiation
+    if (!attr_set) {
+        CK(cudaFuncSetAttribute(chain_kernel<S, WP>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        attr_set = true;
+    }
+    chain_kernel<S, WP><<<grid, CH_NT, bytes, st>>>(P);
+    CK(cudaGetLastError());
+    return HT_OK;
+}
 
 template <typename S>
-int set_smem_attrs(size_t chase_bytes, size_t row_bytes, size_t col_bytes) {
-    CK(cudaFuncSetAttribute(chase_kernel<S, CHASE_NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)chase_bytes));
-    CK(cudaFuncSetAttribute(row_chain_kernel<S, ROW_BM, CHAIN_NT, true>,
-                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)row_bytes));
-    CK(cudaFuncSetAttribute(row_chain_kernel<S, ROW_BM, CHAIN_NT, false>,
-                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)row_bytes));
-    CK(cudaFuncSetAttribute(col_chain_kernel<S, COL_BN, CHAIN_NT>,
-                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)col_bytes));
-    return HT_OK;
+int chain(const ChainParams<S>& P, int WP, int grid, int r, int q, cudaStream_t st) {
+    switch (WP) {
+        case 32: return launch_chain<S, 32>(P, grid, r, q, st);
+        case 64: return launch_chain<S, 64>(P, grid, r, q, st);
+        case 96: return launch_chain<S, 96>(P, grid, r, q, st);
+        case 128: return launch_chain<S, 128>(P, grid, r, q, st);
+        case 160: return launch_chain<S, 160>(P, grid, r, q, st);
+        default: return HT_EUNSUPPORTED;
+    }
+}
+
+template <typename S>
+size_t chain_bytes_rt(int WP, int r, int q) {
+    switch (WP) {
+        case 32: return chain_bytes<S, 32>(r, q);
+        case 64: return chain_bytes<S, 64>(r, q);
+        case 96: return chain_bytes<S, 96>(r, q);
+        case 128: return chain_bytes<S, 128>(r, q);
+        case 160: return chain_bytes<S, 160>(r, q);
+        default: return (size_t)1 << 40;
+    }
 }
 
 template <typename S>
@@ -101,8 +115,7 @@ int run(int64_t n64, int64_t r64, S* H, int64_t ldh, S* T, int64_t ldt, S* Q, in
     }
     const int n = (int)n64;
     const int r = (int)std::min<int64_t>(r64, std::max<int64_t>(1, n64));
-    Timer tm;
-    tm.on = getenv("HT_PROFILE") != nullptr;
+    const bool prof = getenv("HT_PROFILE") != nullptr || (opts && (opts->flags & HT_FLAG_PROFILE));
     cudaEvent_t e_start, e_end;
     CK(cudaEventCreate(&e_start));
     CK(cudaEventCreate(&e_end));
@@ -127,90 +140,92 @@ int run(int64_t n64, int64_t r64, S* H, int64_t ldh, S* T, int64_t ldt, S* Q, in
 
     int64_t q64 = (opts && opts->q > 0) ? opts->q : default_q(n, r, is_complex);
     const int q = (int)std::max<int64_t>(1, std::min<int64_t>(q64, n - 2));
-    const int W = q + r - 1;
+    const int w = q + r - 1;
+    const int WP = (w + 31) / 32 * 32;  // padded window order (DMMA tiles, ring chunks)
+    const int LDB = chain_ldb(WP);
     const int Kmax = 1 + (n - 1 - 2) / r;
-    const size_t chase_bytes = chase_smem_elems<S>(r, W) * sizeof(S);
-    const size_t row_bytes = row_chain_smem<S>(W), col_bytes = col_chain_smem<S>(W);
+    const size_t chase_bytes = chase_smem_elems<S>(r, w) * sizeof(S);
+    const size_t ch_bytes = chain_bytes_rt<S>(WP, r, q);
     int dev = 0, smem_optin = 0, nsm = 0;
     CK(cudaGetDevice(&dev));
     CK(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
     CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-    if (chase_bytes > (size_t)smem_optin || row_bytes > (size_t)smem_optin ||
-        col_bytes > (size_t)smem_optin)
-        return HT_EUNSUPPORTED;
-    if (int rc = set_smem_attrs<S>(chase_bytes, row_bytes, col_bytes)) return rc;
+    if (chase_bytes > (size_t)smem_optin || ch_bytes > (size_t)smem_optin) return HT_EUNSUPPORTED;
+    CK(cudaFuncSetAttribute(chase_kernel<S, CHASE_NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)chase_bytes));
 
     // ---- workspace (stream-ordered) ----
     S *U = nullptr, *V = nullptr, *Zr = nullptr;
     int* prog = nullptr;
-    const size_t blk_elems = (size_t)Kmax * W * W;
+    const size_t blk_elems = (size_t)Kmax * WP * LDB;
     CK(cudaMallocAsync(&U, blk_elems * sizeof(S), stream));
     CK(cudaMallocAsync(&V, blk_elems * sizeof(S), stream));
     CK(cudaMallocAsync(&Zr, (size_t)q * Kmax * (r + 1) * sizeof(S), stream));
     CK(cudaMallocAsync(&prog, (size_t)q * sizeof(int), stream));
 
     const int chase_ctas_req = (opts && opts->chase_ctas > 0) ? opts->chase_ctas : 32;
-    cudaEvent_t ev[8];
-    if (tm.on)
+    // kernel-class timing: 4 events per group from a pool, summed after one sync at the end
+    const int ngroups = (n - 2 + q - 1) / q;
+    std::vector<cudaEvent_t> ev;
+    if (prof) {
+        ev.resize((size_t)4 * ngroups);
         for (auto& e : ev) CK(cudaEventCreate(&e));
-    float ms_chase = 0, ms_ht = 0, ms_qz = 0;
+    }
+    int g = 0;
 
     for (int j1 = 1; j1 <= n - 2; j1 += q) {
         const int qp = std::min(q, n - 1 - j1);
         const int K = 1 + (n - j1 - 2) / r;
-        if (tm.on) CK(cudaEventRecord(ev[0], stream));
-        init_blocks_kernel<S><<<std::min<int64_t>(4 * nsm, ((int64_t)K * W * W + 255) / 256), 256, 0,
-                                stream>>>(U, V, K, W);
+        if (prof) CK(cudaEventRecord(ev[4 * g + 0], stream));
+        init_blocks_kernel<S><<<std::min<int64_t>(4 * nsm, ((int64_t)K * WP * LDB + 255) / 256), 256, 0,
+                                stream>>>(U, V, K, WP, LDB, n, j1, qp + r - 1, r);
         CK(cudaMemsetAsync(prog, 0, (size_t)q * sizeof(int), stream));
-        ChaseArgs<S> ca{n, r, qp, j1, K, W, H, ldh, T, ldt, U, V, Zr, prog};
+        ChaseArgs<S> ca{n, r, qp, j1, K, WP, LDB, H, ldh, T, ldt, U, V, Zr, prog};
         const int P = std::max(1, std::min({qp, chase_ctas_req, nsm}));
         void* kargs[] = {&ca};
         CK(cudaLaunchCooperativeKernel((const void*)chase_kernel<S, CHASE_NT>, dim3(P), dim3(CHASE_NT),
                                        kargs, chase_bytes, stream));
         g_last_launches += 2;
-        if (tm.on) CK(cudaEventRecord(ev[1], stream));
+        if (prof) CK(cudaEventRecord(ev[4 * g + 1], stream));
         // ---- apply phase: right updates of H, T (staircase + V_k), then left (U_k^*) ----
-        ChainArgs<S> ab{n, r, qp, j1, K, W, H, ldh, T, ldt, V, V, Zr, 0};
-        row_chain_kernel<S, ROW_BM, CHAIN_NT, true>
-            <<<dim3((n + ROW_BM - 1) / ROW_BM, 2), CHAIN_NT, row_bytes, stream>>>(ab);
-        ChainArgs<S> lf{n, r, qp, j1, K, W, H, ldh, T, ldt, U, U, nullptr, 0};
-        col_chain_kernel<S, COL_BN, CHAIN_NT>
-            <<<dim3((n + COL_BN - 1) / COL_BN, 2), CHAIN_NT, col_bytes, stream>>>(lf);
+        const int tiles = (n + CH_BM - 1) / CH_BM;
+        ChainParams<S> pr{n, r, qp, j1, K, {{H, ldh, V, CM_AB_RIGHT, 0, tiles}, {T, ldt, V, CM_AB_RIGHT, 0, tiles}},
+                          2, Zr};
+        if (int rc = chain<S>(pr, WP, 2 * tiles, r, q, stream)) return rc;
+        ChainParams<S> pl{n, r, qp, j1, K, {{H, ldh, U, CM_A_LEFT, 1, tiles}, {T, ldt, U, CM_B_LEFT, 1, tiles}},
+                          2, Zr};
+        if (int rc = chain<S>(pl, WP, 2 * tiles, r, q, stream)) return rc;
         g_last_launches += 2;
-        if (tm.on) CK(cudaEventRecord(ev[2], stream));
+        if (prof) CK(cudaEventRecord(ev[4 * g + 2], stream));
         // ---- Q <- Q U_k, Z <- Z V_k (row chains; never read by the chase) ----
         if (Q || Z) {
-            ChainArgs<S> qz{n, r, qp, j1, K, W, Q ? Q : Z, Q ? ldq : ldz, Z ? Z : Q, Z ? ldz : ldq,
-                            Q ? U : V, Z ? V : U, nullptr, 0};
-            row_chain_kernel<S, ROW_BM, CHAIN_NT, false>
-                <<<dim3((n + ROW_BM - 1) / ROW_BM, (Q && Z) ? 2 : 1), CHAIN_NT, row_bytes, stream>>>(qz);
+            ChainParams<S> pq{n, r, qp, j1, K, {{Q ? Q : Z, Q ? ldq : ldz, Q ? U : V, CM_PLAIN, 0, tiles},
+                                                {Z, ldz, V, CM_PLAIN, 0, tiles}},
+                              (Q && Z) ? 2 : 1, Zr};
+            if (int rc = chain<S>(pq, WP, pq.njobs * tiles, r, q, stream)) return rc;
             ++g_last_launches;
         }
         CK(cudaGetLastError());
-        if (tm.on) {
-            CK(cudaEventRecord(ev[3], stream));
-            CK(cudaEventSynchronize(ev[3]));
-            float a = 0, b = 0, c = 0;
-            CK(cudaEventElapsedTime(&a, ev[0], ev[1]));
-            CK(cudaEventElapsedTime(&b, ev[1], ev[2]));
-            CK(cudaEventElapsedTime(&c, ev[2], ev[3]));
-            ms_chase += a;
-            ms_ht += b;
-            ms_qz += c;
-        }
+        if (prof) CK(cudaEventRecord(ev[4 * g + 3], stream));
+        ++g;
     }
     CK(cudaFreeAsync(U, stream));
     CK(cudaFreeAsync(V, stream));
     CK(cudaFreeAsync(Zr, stream));
     CK(cudaFreeAsync(prog, stream));
     CK(cudaEventRecord(e_end, stream));
-    if (tm.on) {
+    if (prof) {
         CK(cudaEventSynchronize(e_end));
         float tot = 0;
         CK(cudaEventElapsedTime(&tot, e_start, e_end));
-        g_last_ms[0] = ms_chase;
-        g_last_ms[1] = ms_ht;
-        g_last_ms[2] = ms_qz;
+        double acc[3] = {0, 0, 0};
+        for (int i = 0; i < g; ++i)
+            for (int c = 0; c < 3; ++c) {
+                float x = 0;
+                CK(cudaEventElapsedTime(&x, ev[4 * i + c], ev[4 * i + c + 1]));
+                acc[c] += x;
+            }
+        for (int c = 0; c < 3; ++c) g_last_ms[c] = acc[c];
         g_last_ms[3] = tot;
         for (auto& e : ev) cudaEventDestroy(e);
     }
