@@ -88,6 +88,20 @@ size_t chain_bytes_rt(int WP, int r, int q) {
     }
 }
 
+// K1 instantiation for the reflector length: the RQ keeps [B_blk; P] in registers on NWR warps
+template <typename S>
+const void* chase_kernel_for(int r) {
+    if constexpr (sizeof(S) == 8) {
+        if (r <= 16) return (const void*)chase_kernel<S, CHASE_NT, 16, 1>;
+        if (r <= 32) return (const void*)chase_kernel<S, CHASE_NT, 32, 1>;
+        if (r <= 64) return (const void*)chase_kernel<S, CHASE_NT, 64, 4>;
+    } else {
+        if (r <= 16) return (const void*)chase_kernel<S, CHASE_NT, 16, 1>;
+        if (r <= 32) return (const void*)chase_kernel<S, CHASE_NT, 32, 2>;
+    }
+    return nullptr;
+}
+
 template <typename S>
 int run(int64_t n64, int64_t r64, S* H, int64_t ldh, S* T, int64_t ldt, S* Q, int64_t ldq, S* Z,
         int64_t ldz, cudaStream_t stream, ncclComm_t comm, const ht_opts* opts, bool is_complex) {
@@ -144,15 +158,20 @@ int run(int64_t n64, int64_t r64, S* H, int64_t ldh, S* T, int64_t ldt, S* Q, in
     const int WP = (w + 31) / 32 * 32;  // padded window order (DMMA tiles, ring chunks)
     const int LDB = chain_ldb(WP);
     const int Kmax = 1 + (n - 1 - 2) / r;
-    const size_t chase_bytes = chase_smem_elems<S>(r, w) * sizeof(S);
+    const int chase_budget = 200 * 1024;
+    const size_t chase_base = chase_smem_elems<S>(r, w, 0) * sizeof(S);
+    const int strip_cap = (int)std::max<int64_t>(0, ((int64_t)chase_budget - (int64_t)chase_base) /
+                                                        (int64_t)((r + 1) * sizeof(S)));
+    const size_t chase_bytes = chase_smem_elems<S>(r, w, strip_cap) * sizeof(S);
+    const void* chase_fn = chase_kernel_for<S>(r);
+    if (!chase_fn || q > 148) return HT_EUNSUPPORTED;  // one co-resident CTA per sweep
     const size_t ch_bytes = chain_bytes_rt<S>(WP, r, q);
     int dev = 0, smem_optin = 0, nsm = 0;
     CK(cudaGetDevice(&dev));
     CK(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
     CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
     if (chase_bytes > (size_t)smem_optin || ch_bytes > (size_t)smem_optin) return HT_EUNSUPPORTED;
-    CK(cudaFuncSetAttribute(chase_kernel<S, CHASE_NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)chase_bytes));
+    CK(cudaFuncSetAttribute(chase_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)chase_bytes));
 
     // ---- workspace (stream-ordered) ----
     S *U = nullptr, *V = nullptr, *Zr = nullptr;
@@ -162,8 +181,13 @@ int run(int64_t n64, int64_t r64, S* H, int64_t ldh, S* T, int64_t ldt, S* Q, in
     CK(cudaMallocAsync(&V, blk_elems * sizeof(S), stream));
     CK(cudaMallocAsync(&Zr, (size_t)q * Kmax * (r + 1) * sizeof(S), stream));
     CK(cudaMallocAsync(&prog, (size_t)q * sizeof(int), stream));
+    long long* k1prof = nullptr;  // HT_K1PROF=1: chase phase cycle counts (stderr)
+    const bool k1p = getenv("HT_K1PROF") != nullptr;
+    if (k1p) {
+        CK(cudaMallocAsync(&k1prof, 8 * sizeof(long long), stream));
+        CK(cudaMemsetAsync(k1prof, 0, 8 * sizeof(long long), stream));
+    }
 
-    const int chase_ctas_req = (opts && opts->chase_ctas > 0) ? opts->chase_ctas : 32;
     // kernel-class timing: 4 events per group from a pool, summed after one sync at the end
     const int ngroups = (n - 2 + q - 1) / q;
     std::vector<cudaEvent_t> ev;
@@ -180,11 +204,9 @@ int run(int64_t n64, int64_t r64, S* H, int64_t ldh, S* T, int64_t ldt, S* Q, in
         init_blocks_kernel<S><<<std::min<int64_t>(4 * nsm, ((int64_t)K * WP * LDB + 255) / 256), 256, 0,
                                 stream>>>(U, V, K, WP, LDB, n, j1, qp + r - 1, r);
         CK(cudaMemsetAsync(prog, 0, (size_t)q * sizeof(int), stream));
-        ChaseArgs<S> ca{n, r, qp, j1, K, WP, LDB, H, ldh, T, ldt, U, V, Zr, prog};
-        const int P = std::max(1, std::min({qp, chase_ctas_req, nsm}));
+        ChaseArgs<S> ca{n, r, qp, j1, K, WP, LDB, H, ldh, T, ldt, U, V, Zr, prog, strip_cap, k1prof};
         void* kargs[] = {&ca};
-        CK(cudaLaunchCooperativeKernel((const void*)chase_kernel<S, CHASE_NT>, dim3(P), dim3(CHASE_NT),
-                                       kargs, chase_bytes, stream));
+        CK(cudaLaunchCooperativeKernel(chase_fn, dim3(qp), dim3(CHASE_NT), kargs, chase_bytes, stream));
         g_last_launches += 2;
         if (prof) CK(cudaEventRecord(ev[4 * g + 1], stream));
         // ---- apply phase: right updates of H, T (staircase + V_k), then left (U_k^*) ----
@@ -213,6 +235,18 @@ int run(int64_t n64, int64_t r64, S* H, int64_t ldh, S* T, int64_t ldt, S* Q, in
     CK(cudaFreeAsync(V, stream));
     CK(cudaFreeAsync(Zr, stream));
     CK(cudaFreeAsync(prog, stream));
+    if (k1p) {
+        long long h[8];
+        CK(cudaMemcpyAsync(h, k1prof, sizeof(h), cudaMemcpyDeviceToHost, stream));
+        CK(cudaStreamSynchronize(stream));
+        const char* nm[8] = {"wait", "loads", "catchup", "larfg+QB", "RQ||U", "strip+V", "RQonly", "loop"};
+        double tot = 0;
+        for (long long x : h) tot += (double)x;
+        fprintf(stderr, "K1 cycles (sum over CTAs):");
+        for (int i = 0; i < 8; ++i) fprintf(stderr, " %s=%.1f%%", nm[i], 100.0 * h[i] / tot);
+        fprintf(stderr, " total=%.3g\n", tot);
+        CK(cudaFreeAsync(k1prof, stream));
+    }
     CK(cudaEventRecord(e_end, stream));
     if (prof) {
         CK(cudaEventSynchronize(e_end));

@@ -70,6 +70,10 @@ __device__ __forceinline__ double shfl_xor(double v, int m) { return __shfl_xor_
 __device__ __forceinline__ zc shfl_xor(zc v, int m) {
     return zc(__shfl_xor_sync(0xffffffffu, v.x, m), __shfl_xor_sync(0xffffffffu, v.y, m));
 }
+__device__ __forceinline__ double shfl_idx(double v, int l) { return __shfl_sync(0xffffffffu, v, l); }
+__device__ __forceinline__ zc shfl_idx(zc v, int l) {
+    return zc(__shfl_sync(0xffffffffu, v.x, l), __shfl_sync(0xffffffffu, v.y, l));
+}
 template <typename S>
 __device__ __forceinline__ S warp_sum(S v) {
 #pragma unroll
