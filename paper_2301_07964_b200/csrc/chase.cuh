@@ -6,22 +6,16 @@
 // Per step (j,k), 1-based as in the paper:
 //   jb = j + max(0,(k-1)r+1), i1 = j+kr+1, i2 = min(j+(k+1)r,n), i3 = min(j+(k+2)r,n),
 //   i4 = j1 + 1 + max(0,(k+j-j1-q+1)r)                                 (corrected, c8)
-//   (a) catch-up of Q_k^{j1..j-1} on A(.,jb) and B(.,i1+r-1)  (Alg. 3 lines 9-16) as ONE
-//       mat-vec with the partial product U_k = Q_k^{j1}...Q_k^{j-1} (kept dense; K2 fused)
+//   (a) catch-up of Q_k^{j1..j-1} on A(.,jb) and B(.,i1+r-1)  (Alg. 3 lines 9-16), applied in
+//       compact-WY form U_k^* x = x - Y T^* Y^* x (three parallel rounds instead of a chain of
+//       t reflector applications); sweep j appends column t of window k's T factor (xLARFT)
 //   (b) Q_k^j reduces A(i1:i2,jb); B(i1:i2,i1:i2) <- Q^* B           (lines 17-19)
-//   (c) RQ of B(i1:i2,i1:i2); Z_k^j from the first row of Q~          (lines 20-21)
+//   (c) Householder RQ of B(i1:i2,i1:i2) (xGERQ2 order, reading c4); the first row of Q~
+//       comes out of the [C; P] stacked rows (P accumulates H_{m-1}...H_1 so P e1 = Q~^* e1);
+//       Z_k^j = larfg(conj(Q~(1,:))^T)                                 (lines 20-21, c3)
 //   (d) A(i4:i3,i1:i2) <- A Z ; B(i4:i2,i1:i2) <- B Z                   (lines 22-23)
-//   U_k <- U_k Q_k^j and V_k <- V_k Z_k^j ("Form compact WY", kept as
-//   dense w x w blocks for the DMMA chains); Z_k^j stored for the staircase (K4).
-//
-// Latency design: every input of a step is final once (j-1,k+2) is done, except column jb,
-// which the same CTA produced in step k-1 and keeps in shared memory; so a step issues all
-// of its loads at once (cp.async: U_k, V_k, the B block and catch-up column, and as much of
-// the tall strip as fits), then runs a chain of one-reduction phases.  The RQ runs on
-// NWR warps with the stacked [B_blk; P] rows in registers (one row per lane slot): each
-// Householder stage broadcasts row i through shared memory and needs ONE reduction-free
-// pass (all dot products with row i at once, the norm included), P accumulating
-// H_m...H_2 so that P e1 = Q~^* e1 comes out without a second sweep.
+// The reflectors (v, tau) of Q_k^j and Z_k^j are stored as records; K2 (accum.cuh) folds them
+// into the dense window blocks U_k, V_k for the apply phase.
 #pragma once
 #include "scalar.cuh"
 
@@ -31,14 +25,15 @@
 
 template <typename S>
 struct ChaseArgs {
-    int n, r, qp, j1, K, WP, LDB;
+    int n, r, qp, j1, K;
     S* A;
     int64_t lda;
     S* B;
     int64_t ldb;
-    S* U;       // K dense blocks, row-major: (l, c) at U[k*WP*LDB + l*LDB + c]
-    S* V;       // (rows/cols >= w_k are zero; U_k, V_k start as I_{w_k})
-    S* Zr;      // (qp*K) records of (r+1): Z_k^j vector (m entries), sigma at [r]
+    S* Qr;      // (qp*K) records of (r+1): v of Q_k^j (v[0]=1, m entries), tau at [r]
+    S* Zr;      // (qp*K) records of (r+1): v of Z_k^j, sigma at [r]
+    S* Tr;      // (qp*K) records of TLD: column t of window k's WY factor T (rows 0..t)
+    int TLD;
     int* prog;  // qp counters: steps completed by each sweep of the group
     int strip_cap;  // strip rows (A then B) staged in shared memory per step
     long long* prof;  // optional: per-CTA cycle counts of the step phases (8 slots)
@@ -47,6 +42,11 @@ struct ChaseArgs {
 __device__ __forceinline__ int ld_acquire(const int* p) {
     int v;
     asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ int ld_relaxed(const int* p) {
+    int v;
+    asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
 __device__ __forceinline__ void st_release(int* p, int v) {
@@ -61,6 +61,19 @@ template <typename S>
 __device__ __forceinline__ void k1_ld(S* s, const S* g) { k1_cp_async(s, g, (int)sizeof(S)); }
 __device__ __forceinline__ void k1_commit_wait() {
     asm volatile("cp.async.commit_group;\ncp.async.wait_all;\n" ::: "memory");
+}
+// Stage flag of the RQ's two warp groups.  The producer publishes after a named barrier that
+// orders every producer thread's ring writes before the flag store; shared-memory stores of one
+// SM are performed in issue order, so a volatile store suffices (no MEMBAR on the RQ chain).
+__device__ __forceinline__ void st_release_cta(volatile int* p, int v) {
+    const unsigned a = (unsigned)__cvta_generic_to_shared((const void*)p);
+    asm volatile("st.volatile.shared.s32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ int ld_acquire_cta(volatile int* p) {
+    const unsigned a = (unsigned)__cvta_generic_to_shared((const void*)p);
+    int v;
+    asm volatile("ld.volatile.shared.s32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+    return v;
 }
 __device__ __forceinline__ void named_bar(int id, int nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
@@ -91,132 +104,231 @@ __device__ __forceinline__ void warp_larfg(int m, const S* x, S* vout, S& tau, d
     __syncwarp();
 }
 
-// RQ-based opposite reflector direction (readings c3/c4) on NWR warps.
-// In: Cb (m x m, col-major, ld LDC) = B(i1:i2,i1:i2) after Q_k^j.  Out: uu[0..m) = Q~^* e1.
-// Householder RQ, rows bottom-up (xGERQ2 order): stage i uses h = scal*(conj(row_i) - beta e_i)
-// (h_i = 1), so every row's dot with h is scal*(g_l - beta*C[l,i]) with g_l = <row_l, row_i>:
-// one pass per stage.  Rows of P (= H_m...H_2 accumulated, P e1 = Q~^* e1) ride along.
-template <typename S, int MAXM, int NWR>
-__device__ __forceinline__ void rq_direction(int m, const S* Cb, int LDC, S* bc, S* uu) {
-    constexpr int ROWS = 32 * NWR;
-    constexpr int RPL = (2 * MAXM + ROWS - 1) / ROWS;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    S row[RPL][MAXM];
-    int rho[RPL];
+// RQ thread layout.  Group A (threads [0, NA)) holds the m rows of C, group B (threads
+// [NA, 2NA)) the m rows of P; LPR threads per row, each with E columns in REGISTERS, columns
+// interleaved (thread part p holds columns LPR*e + p) so that the per-stage skip of the columns
+// a stage does not touch (H_i acts on columns 0..i) is warp-uniform, in sub-blocks of SB.
+// Group A carries the sequential chain (pivot rows, scalars); group B only consumes each stage's
+// pivot row and scalars from a shared-memory ring and trails it (never blocks group A).
+template <typename S, int MAXM>
+struct RQCfg {
+    static constexpr int LPR = (MAXM >= 16) ? 2 : 1;
+    static constexpr int E = MAXM / LPR;
+    static constexpr int SB = 8;
+    static constexpr int NSB = (E + SB - 1) / SB;
+    static constexpr int ROWT = MAXM * LPR;
+    static constexpr int NA = (ROWT < 32) ? 32 : ROWT;
+    static constexpr int NTHR = 2 * NA;
+    static constexpr int PLD = LPR * NSB * SB + 4;  // ring slot: pivot row (de-interleaved) + K1, K2
+};
+
+template <typename S, int LPR>
+__device__ __forceinline__ S lpr_sum(S v) {
 #pragma unroll
-    for (int s = 0; s < RPL; ++s) {
-        rho[s] = s * ROWS + warp * 32 + lane;
+    for (int o = 1; o < LPR; o <<= 1) v += shfl_xor(v, o);
+    return v;
+}
+
+// Householder RQ (readings c3/c4), rows bottom-up (xGERQ2 order) on C = B(i1:i2,i1:i2) (m x m,
+// col-major, ld LDC) with P = I alongside.  Stage i (i = m-1 .. 1, plus 0 for complex) generates
+// H_i from row i of C (alpha = conj(C[i][i]), tail conj(C[i][0..i)): oracle_rq_first_row's larfg)
+// and right-multiplies C rows 0..i-1 and all P rows by H_i on columns 0..i.  Then
+// P = H_{m-1}...H_0 = Q~^*, and uu = P e1 = Q~^* e1 = conj(Q~(1,:))^T.
+// Per row: g = sum_{c<i} row[c] conj(C[i][c]), ri = row[i];  row[c] -= f C[i][c] (c < i) with
+// f = K1 (g + K2 ri), K1 = tau |1/(alpha-beta)|^2, K2 = alpha - beta (real: K1 = 1/(s + |alpha| nrm),
+// s = |alpha|^2 + |tail|^2).  Column i is dead after stage i (later stages act on columns < i,
+// the output is column 0), so it is not updated.  ring: m slots of PLD; flag: volatile counter.
+template <typename S, int MAXM>
+__device__ __forceinline__ void rq_direction(int m, const S* Cb, int LDC, S* ring, volatile int* flag, S* uu) {
+    using CF = RQCfg<S, MAXM>;
+    constexpr int LPR = CF::LPR, E = CF::E, SB = CF::SB, NSB = CF::NSB, NA = CF::NA, PLD = CF::PLD;
+    constexpr int EP = NSB * SB;  // padded elements per thread
+    const int tid = threadIdx.x;
+    const bool grpB = tid >= NA;
+    const int gt = grpB ? tid - NA : tid;
+    const int l = gt / LPR, part = gt % LPR;
+    const bool live = gt < CF::ROWT && l < m;
+    S row[EP];
 #pragma unroll
-        for (int c = 0; c < MAXM; ++c) {
-            S v = S(0.0);
-            if (c < m) {
-                if (rho[s] < m) v = Cb[rho[s] + c * LDC];
-                else if (rho[s] < 2 * m) v = S((rho[s] - m) == c ? 1.0 : 0.0);
-            }
-            row[s][c] = v;
-        }
+    for (int e = 0; e < EP; ++e) {
+        const int c = LPR * e + part;
+        S v = S(0.0);
+        if (live && e < E && c < m) v = grpB ? S(l == c ? 1.0 : 0.0) : Cb[l + c * LDC];
+        row[e] = v;
     }
-    int par = 0;
-    for (int i = m - 1; i >= 1; --i) {
-        // broadcast row i of C (its owner: slot i / ROWS, warp (i % ROWS) / 32, lane i % 32)
-        S b[MAXM];
-        if (NWR == 1) {
-            const int src = i & 31, sl = i / ROWS;
+    auto syncA = [&]() {
+        if (NA <= 32) __syncwarp();
+        else named_bar(1, NA);
+    };
+    auto write_pivot = [&](int slot, int upto) {  // this thread's chunk of its row into ring slot
+        S* dst = ring + (size_t)slot * PLD + part * EP;
 #pragma unroll
-            for (int c = 0; c < MAXM; ++c) {
-                S v = row[0][c];
+        for (int sb = 0; sb < NSB; ++sb)
+            if (sb * SB * LPR < upto)
 #pragma unroll
-                for (int s = 1; s < RPL; ++s)
-                    if (sl == s) v = row[s][c];
-                b[c] = shfl_idx(v, src);
-            }
-        } else {
-            S* bs = bc + par * (MAXM + 1);
+                for (int e = 0; e < SB; ++e) dst[sb * SB + e] = row[sb * SB + e];
+    };
+    // per-stage local work: g, nx (partial over my columns < i), ri
+    S bk[EP];
+    auto dots = [&](const S* pv, int i, S& g, double& nx, S& ri) {
+        const int eth = (i - part + LPR - 1) / LPR;  // my elements e < eth have column < i
+        const int sbi = eth / SB;
+        double n0 = 0.0, n1 = 0.0;
+        S g0 = S(0.0), g1 = S(0.0);
+        ri = S(0.0);
+        const int ei = (i % LPR == part) ? i / LPR : -1;
 #pragma unroll
-            for (int s = 0; s < RPL; ++s)
-                if (rho[s] == i) {
+        for (int sb = 0; sb < NSB; ++sb) {
+            if (sb * SB * LPR <= i) {  // uniform: the block holds columns <= i for some part
 #pragma unroll
-                    for (int c = 0; c < MAXM; ++c) bs[c] = row[s][c];
-                }
-            named_bar(1, 32 * NWR);
-#pragma unroll
-            for (int c = 0; c < MAXM; ++c) b[c] = bs[c];
-        }
-        // scalars of stage i (every lane redundantly): alpha = conj(C[i,i]), x = conj(C[i,0:i))
-        double n4[4] = {0.0, 0.0, 0.0, 0.0};
-        S bi = S(0.0);
-#pragma unroll
-        for (int c = 0; c < MAXM; ++c) {
-            if (c < i) n4[c & 3] += abs2(b[c]);
-            if (c == i) bi = b[c];
-        }
-        const double nx = (n4[0] + n4[1]) + (n4[2] + n4[3]);
-        const S alpha = conjv(bi);
-        if (!(nx == 0.0 && im(alpha) == 0.0)) {
-            const double nrm = sqrt(abs2(alpha) + nx);
-            const double beta = (re(alpha) >= 0.0) ? -nrm : nrm;
-            // tau |scal|^2 = ((beta-alpha)/beta) / |alpha-beta|^2 = -1 / (beta conj(alpha-beta))
-            const S ts = -recip(beta * conjv(alpha - S(beta)));
-            // rows >= i of C are finished (never read again), so they may be updated too:
-            // every lane runs the same straight-line code (no divergence)
-#pragma unroll
-            for (int s = 0; s < RPL; ++s) {
-                S g4[4] = {S(0.0), S(0.0), S(0.0), S(0.0)};
-                S cli = S(0.0);
-#pragma unroll
-                for (int c = 0; c < MAXM; ++c) {
-                    const S bc_ = (c <= i) ? b[c] : S(0.0);
-                    g4[c & 3] = fma_s(row[s][c], conjv(bc_), g4[c & 3]);
-                    if (c == i) cli = row[s][c];
-                }
-                const S coef = ts * (((g4[0] + g4[1]) + (g4[2] + g4[3])) - beta * cli);
-#pragma unroll
-                for (int c = 0; c < MAXM; ++c) {
-                    const S d = (c < i) ? b[c] : ((c == i) ? b[c] - S(beta) : S(0.0));
-                    row[s][c] -= coef * d;
+                for (int e = 0; e < SB; ++e) {
+                    const int ee = sb * SB + e;
+                    const S b = (ee < eth) ? pv[part * EP + ee] : S(0.0);
+                    bk[ee] = b;
+                    if (e & 1) {
+                        n1 += abs2(b);
+                        g1 = fma_s(row[ee], conjv(b), g1);
+                    } else {
+                        n0 += abs2(b);
+                        g0 = fma_s(row[ee], conjv(b), g0);
+                    }
+                    if (ee == ei) ri = row[ee];
                 }
             }
         }
-        par ^= 1;
+        (void)sbi;
+        g = g0 + g1;
+        nx = n0 + n1;
+    };
+    auto update = [&](int i, S f) {  // bk (zero for columns >= i) from dots()
+#pragma unroll
+        for (int sb = 0; sb < NSB; ++sb) {
+            if (sb * SB * LPR <= i) {
+#pragma unroll
+                for (int e = 0; e < SB; ++e) row[sb * SB + e] -= f * bk[sb * SB + e];
+            }
+        }
+    };
+    const int ilast = (sizeof(S) == 8) ? 1 : 0;
+    if (!grpB) {
+        // ---------------- group A: C rows, the sequential chain ----------------
+        if (live && l == m - 1) write_pivot(m - 1, m);
+        syncA();
+        for (int i = m - 1; i >= 1; --i) {
+            const S* pv = ring + (size_t)i * PLD;
+            const S alpha = conjv(pv[(i % LPR) * EP + i / LPR]);
+            S g, ri;
+            double nx;
+            dots(pv, i, g, nx, ri);
+            nx = lpr_sum<double, LPR>(nx);
+            g = lpr_sum<S, LPR>(g);
+            ri = lpr_sum<S, LPR>(ri);
+            S K1 = S(0.0), K2 = S(0.0);
+            if (!(nx == 0.0 && im(alpha) == 0.0)) {  // uniform
+                const double s2 = abs2(alpha) + nx;
+                const double nrm = sqrt(s2);
+                const double beta = (re(alpha) >= 0.0) ? -nrm : nrm;
+                K2 = alpha - S(beta);
+                if constexpr (sizeof(S) == 8) {
+                    K1 = S(1.0 / (s2 + fabs(re(alpha)) * nrm));
+                } else {
+                    const S tau = (S(beta) - alpha) * (1.0 / beta);
+                    K1 = tau * (1.0 / abs2(K2));
+                }
+            }
+            S f = K1 * (g + K2 * ri);
+            if (!(live && l < i)) f = S(0.0);
+            update(i, f);
+            if (gt == 0) {
+                ring[(size_t)i * PLD + LPR * EP] = K1;
+                ring[(size_t)i * PLD + LPR * EP + 1] = K2;
+            }
+            if (live && l == i - 1) write_pivot(i - 1, i);
+            syncA();
+            if (gt == 0) st_release_cta(flag, i);  // stage i (pivot, K1, K2) complete
+        }
+        if constexpr (sizeof(S) != 8) {
+            // stage 0: H_0 = I - tau e1 e1^* makes R~(0,0) real; P rows get row[0] *= (1 - tau)
+            const S alpha = conjv(ring[0 * PLD]);
+            S tau = S(0.0);
+            if (im(alpha) != 0.0) {
+                const double nrm = sqrt(abs2(alpha));
+                const double beta = (re(alpha) >= 0.0) ? -nrm : nrm;
+                tau = (S(beta) - alpha) * (1.0 / beta);
+            }
+            if (gt == 0) {
+                ring[LPR * EP] = tau;
+                st_release_cta(flag, 0);
+            }
+        }
+    } else {
+        // ---------------- group B: P rows, trailing consumer ----------------
+        for (int i = m - 1; i >= ilast; --i) {
+            while (ld_acquire_cta(flag) > i) {
+            }
+            const S* pv = ring + (size_t)i * PLD;
+            const S K1 = pv[LPR * EP], K2 = pv[LPR * EP + 1];
+            if (i == 0) {  // complex stage 0 (see group A)
+                if (live && part == 0) row[0] -= K1 * row[0];
+                continue;
+            }
+            S g, ri;
+            double nx;
+            dots(pv, i, g, nx, ri);
+            g = lpr_sum<S, LPR>(g);
+            ri = lpr_sum<S, LPR>(ri);
+            S f = K1 * (g + K2 * ri);
+            if (!live) f = S(0.0);
+            update(i, f);
+        }
+        if (live && part == 0) uu[l] = row[0];
     }
-#pragma unroll
-    for (int s = 0; s < RPL; ++s)
-        if (rho[s] >= m && rho[s] < 2 * m) uu[rho[s] - m] = row[s][0];
 }
 
 template <typename S>
-__host__ __device__ inline size_t chase_smem_elems(int r, int w, int strip_cap) {
-    // xcol (2 buffers), ys, tx/ty, U, V (w x (w+1)), Cb r x (r+1), vectors, strip
-    return 2 * (size_t)(w + r + 8) + (size_t)(w + r + 8) + 2 * (size_t)(w + r + 8) +
-           2 * (size_t)w * (w + 1) + (size_t)r * (r + 1) + 4 * (size_t)(r + 8) + 2 * (size_t)(r + 9) +
-           16 + (size_t)strip_cap * (r + 1);
+__host__ __device__ inline size_t chase_smem_elems(int r, int qp, int strip_cap) {
+    const int w = qp + r - 1;
+    const size_t XL = (size_t)(w + r + 8);
+    return 3 * XL +                      // x (2 buffers), y
+           (size_t)r * (r + 1) +         // B block
+           3 * (size_t)(r + 8) +         // vq, vz, uu
+           (size_t)r * (r + 20) +        // RQ ring (pivot rows + scalars per stage)
+           16 +                          // scalars
+           (size_t)qp * (r + 1) +        // catch-up records (Y)
+           (size_t)qp * (qp + 1) +       // T factor of window k
+           5 * (size_t)(qp + 8) +        // WY temporaries
+           (size_t)strip_cap * (r + 1);  // staged strip rows
 }
 
-template <typename S, int NT, int MAXM, int NWR>
+template <typename S, int NT, int MAXM>
 __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
     extern __shared__ __align__(16) unsigned char smraw[];
     S* sm = reinterpret_cast<S*>(smraw);
-    const int n = a.n, r = a.r, qp = a.qp, j1 = a.j1, K = a.K, LDB = a.LDB;
+    const int n = a.n, r = a.r, qp = a.qp, j1 = a.j1, K = a.K;
     const int w = qp + r - 1;
-    const int LU = (w & 1) ? w : w + 1;  // odd ld of the U/V copies (conflict-free rows)
-    const int SLD = r + 1;               // odd-ish ld of the strip rows
+    const int SLD = r + 1;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     constexpr int NW = NT / 32;
     const int XL = w + r + 8;
+    const int TL = qp + 1;
     S* xc[2] = {sm, sm + XL};  // column jb of this step / of the next step
     S* ys = sm + 2 * XL;
-    S* tx = ys + XL;
-    S* ty = tx + XL;
-    S* Ub = ty + XL;           // U_k rows/cols [0, t+m)
-    S* Vb = Ub + (size_t)w * LU;
-    S* Cb = Vb + (size_t)w * LU;  // r x (r+1)
+    S* Cb = ys + XL;           // r x (r+1) col-major
     S* vq = Cb + (size_t)r * (r + 1);
     S* vz = vq + (r + 8);
     S* uu = vz + (r + 8);
-    S* xs2 = uu + (r + 8);     // spare
-    S* bc = xs2 + (r + 8);     // 2 x (r+9) RQ broadcast rows
-    S* scal = bc + 2 * (r + 9);  // 16 scalars
-    S* strip = scal + 16;      // strip_cap rows x (r+1) (row-major)
+    S* ring = uu + (r + 8);    // RQ ring: r x (r+20)
+    S* scal = ring + (size_t)r * (r + 20);
+    __shared__ int rq_flag;
+    if (threadIdx.x == 0) rq_flag = 1 << 30;
+    S* rec = scal + 16;        // qp x (r+1): v of Q_k^{j1+s}, tau at [r]
+    S* Tsm = rec + (size_t)qp * (r + 1);  // T(p, s) at Tsm[p*TL + s]
+    S* wx = Tsm + (size_t)qp * TL;        // Y^* x, then T^* Y^* x
+    S* wy = wx + (qp + 8);
+    S* zx = wy + (qp + 8);
+    S* zy = zx + (qp + 8);
+    S* wu = zy + (qp + 8);                // Y^* v (T column build)
+    S* strip = wu + (qp + 8);  // strip_cap rows x (r+1) (row-major)
     const int LDC = r + 1;
     const int t = blockIdx.x;
     if (t >= qp) return;
@@ -224,7 +336,7 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
     const int kcount = min(K, 2 + (n - j - 1) / r);
     const int kprev = (t > 0) ? min(K, 2 + (n - j) / r) : 0;
     int cur = 0;
-    long long pt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    long long pt[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
     long long tc = clock64();
 #define K1_TICK(slot)                         \
     do {                                      \
@@ -233,11 +345,13 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
         tc = now_;                            \
     } while (0)
     for (int k = 0; k < kcount; ++k) {
-        K1_TICK(7);
         if (t > 0) {
             if (tid == 0) {
                 const int need = min(k + 3, kprev);
-                while (ld_acquire(&a.prog[t - 1]) < need) {
+                if (ld_acquire(&a.prog[t - 1]) < need) {
+                    while (ld_relaxed(&a.prog[t - 1]) < need) {
+                    }
+                    (void)ld_acquire(&a.prog[t - 1]);
                 }
             }
             __syncthreads();
@@ -254,97 +368,104 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
         const int nx = i2 - b0 + 1;
         const int cB = i1 + r - 1;  // == i2 when it exists
         const bool hasB = cB <= n;
-        const int tm = t + max(m, 0);  // U/V square needed: [0, t+m)
-        S* Uk = a.U + (int64_t)k * a.WP * LDB;
-        S* Vk = a.V + (int64_t)k * a.WP * LDB;
         S* xcol = xc[cur];
         S* xnext = xc[cur ^ 1];
         const int nA = max(0, i3 - i4 + 1), nBs = max(0, i1 - i4);  // strip rows (B: above block)
         const int stA = min(nA, a.strip_cap), stB = min(nBs, a.strip_cap - stA);
         const bool gen = (m >= 2) && jb <= n && nx > 0;
+        const bool cu = (t > 0) && L >= 1 && jb <= n && nx > 0;  // catch-up present
         // ---- (S1) all loads of the step at once ------------------------------------------
         if (jb <= n && nx > 0) {
             if (k == 0)
                 for (int i = tid; i < nx; i += NT) k1_ld(&xcol[i], &IDX(a.A, a.lda, b0 + i, jb));
             if (hasB)
                 for (int i = tid; i < nx; i += NT) k1_ld(&ys[i], &IDX(a.B, a.ldb, b0 + i, cB));
-            if (t > 0)
-                for (int e = tid; e < tm * tm; e += NT) {
-                    const int l = e / tm, c = e % tm;
-                    k1_ld(&Ub[l * LU + c], &Uk[(int64_t)l * LDB + c]);
+            if (cu) {  // warp per record / per T column (no integer division in the loops)
+                for (int s2 = warp; s2 < t; s2 += NW) {
+                    const S* src = a.Qr + ((int64_t)s2 * K + k) * (r + 1);
+                    for (int c = lane; c <= r; c += 32) k1_ld(&rec[s2 * (r + 1) + c], src + c);
+                    const S* tsrc = a.Tr + ((int64_t)s2 * K + k) * a.TLD;
+                    for (int p = lane; p <= s2; p += 32) k1_ld(&Tsm[p * TL + s2], tsrc + p);
                 }
+            }
             if (gen) {
-                if (t > 0)
-                    for (int e = tid; e < tm * tm; e += NT) {
-                        const int l = e / tm, c = e % tm;
-                        k1_ld(&Vb[l * LU + c], &Vk[(int64_t)l * LDB + c]);
-                    }
-                for (int e = tid; e < m * m; e += NT) {
-                    const int ii = e % m, cc = e / m;
-                    k1_ld(&Cb[ii + cc * LDC], &IDX(a.B, a.ldb, i1 + ii, i1 + cc));
-                }
-                for (int e = tid; e < (stA + stB) * m; e += NT) {
-                    const int rr = e % (stA + stB), cc = e / (stA + stB);
-                    const S* src = rr < stA ? &IDX(a.A, a.lda, i4 + rr, i1 + cc)
-                                            : &IDX(a.B, a.ldb, i4 + (rr - stA), i1 + cc);
-                    k1_ld(&strip[rr * SLD + cc], src);
+                for (int cc = warp; cc < m; cc += NW) {
+                    for (int ii = lane; ii < m; ii += 32) k1_ld(&Cb[ii + cc * LDC], &IDX(a.B, a.ldb, i1 + ii, i1 + cc));
+                    for (int rr = lane; rr < stA; rr += 32) k1_ld(&strip[rr * SLD + cc], &IDX(a.A, a.lda, i4 + rr, i1 + cc));
+                    for (int rr = lane; rr < stB; rr += 32)
+                        k1_ld(&strip[(stA + rr) * SLD + cc], &IDX(a.B, a.ldb, i4 + rr, i1 + cc));
                 }
             }
         }
-        if (t == 0 && gen)
-            for (int e = tid; e < tm * tm; e += NT) {
-                const int l = e / tm, c = e % tm;
-                Ub[l * LU + c] = S(l == c ? 1.0 : 0.0);
-                Vb[l * LU + c] = S(l == c ? 1.0 : 0.0);
-            }
         k1_commit_wait();
         __syncthreads();
         K1_TICK(1);
         if (jb <= n && nx > 0) {
-            // ---- (S2) catch-up: x(0:L) <- U^* x(0:L), same for the B column --------------------
-            if (L >= 1) {
-                for (int o = tid; o < L; o += NT) {
-                    S s0 = S(0.0), s1 = S(0.0), y0 = S(0.0), y1 = S(0.0);
-                    int l = 0;
-                    for (; l + 1 < L; l += 2) {
-                        const S u0 = Ub[l * LU + o], u1 = Ub[(l + 1) * LU + o];
-                        s0 += conj_mul(u0, xcol[l]);
-                        s1 += conj_mul(u1, xcol[l + 1]);
-                        if (hasB) {
-                            y0 += conj_mul(u0, ys[l]);
-                            y1 += conj_mul(u1, ys[l + 1]);
-                        }
+            // ---- (S2) catch-up in WY form: x(0:L) <- x - Y T^* Y^* x (same for y) ----------------
+            if (cu) {
+                // round 1: w_s = Y(:,s)^* x, s < t (thread per (vector, s))
+                for (int e = tid; e < 2 * t; e += NT) {
+                    const int s = e % t;
+                    const bool isy = e >= t;
+                    if (isy && !hasB) continue;
+                    const S* v = rec + (size_t)s * (r + 1);
+                    const S* xv = isy ? ys : xcol;
+                    const int ms = min(r, n - (j1 + s + k * r));
+                    S d0 = S(0.0), d1 = S(0.0);
+                    int i = 0;
+                    for (; i + 1 < ms; i += 2) {
+                        d0 += conj_mul(v[i], xv[s + i]);
+                        d1 += conj_mul(v[i + 1], xv[s + i + 1]);
                     }
-                    if (l < L) {
-                        const S u0 = Ub[l * LU + o];
-                        s0 += conj_mul(u0, xcol[l]);
-                        if (hasB) y0 += conj_mul(u0, ys[l]);
-                    }
-                    tx[o] = s0 + s1;
-                    ty[o] = y0 + y1;
+                    if (i < ms) d0 += conj_mul(v[i], xv[s + i]);
+                    if (is_zero(v[r])) d0 = d1 = S(0.0);  // tau = 0: Q = I (record may be empty)
+                    (isy ? wy : wx)[s] = d0 + d1;
                 }
                 __syncthreads();
-                for (int i = tid; i < L; i += NT) {
-                    xcol[i] = tx[i];
-                    if (hasB) ys[i] = ty[i];
+                // round 2: z = T^* w  (z_s = sum_{p<=s} conj(T(p,s)) w_p)
+                for (int e = tid; e < 2 * t; e += NT) {
+                    const int s = e % t;
+                    const bool isy = e >= t;
+                    if (isy && !hasB) continue;
+                    const S* wv = isy ? wy : wx;
+                    S z = S(0.0);
+                    for (int p = 0; p <= s; ++p) z += conj_mul(Tsm[p * TL + s], wv[p]);
+                    (isy ? zy : zx)[s] = z;
                 }
-                if (hasB && gen) {  // catch-up column also feeds the block and the B strip
-                    for (int i = tid; i < t && i < L; i += NT) {
-                        const int rr = (b0 + i) - i4;  // strip row of B row b0+i (>= 0)
-                        if (rr >= 0 && rr < stB) strip[(stA + rr) * SLD + (m - 1)] = ty[i];
+                __syncthreads();
+                // round 3: x(i) -= sum_s Y(i,s) z_s over reflectors covering row i
+                for (int e = tid; e < 2 * L; e += NT) {
+                    const int i = e % L;
+                    const bool isy = e >= L;
+                    if (isy && !hasB) continue;
+                    const S* z = isy ? zy : zx;
+                    S acc = S(0.0);
+                    const int slo = max(0, i - r + 1), shi = min(t - 1, i);
+                    for (int s = slo; s <= shi; ++s) {
+                        const int ms = min(r, n - (j1 + s + k * r));
+                        if (i - s < ms) acc += rec[(size_t)s * (r + 1) + (i - s)] * z[s];
                     }
+                    (isy ? ys : xcol)[i] -= acc;
+                }
+                __syncthreads();
+                if (hasB && gen) {
                     for (int i = tid; i < m; i += NT)
-                        if (t + i < L) Cb[i + (m - 1) * LDC] = ty[t + i];
+                        if (t + i < L) Cb[i + (m - 1) * LDC] = ys[t + i];
+                    // caught-up rows b0..i1-1 of column i2 are also rows of the staged B strip
+                    for (int i = tid; i < t && i < L; i += NT) {
+                        const int rr = (b0 + i) - i4;
+                        if (rr >= 0 && rr < stB) strip[(stA + rr) * SLD + (m - 1)] = ys[i];
+                    }
                 }
-                __syncthreads();
             }
-            if (hasB && gen && !(L >= 1))
+            if (hasB && gen && !cu)
                 for (int i = tid; i < m; i += NT) Cb[i + (m - 1) * LDC] = ys[t + i];
             if (!gen) {  // catch-up only (no reflector at this step; Alg. 2 has m >= 2)
                 for (int i = tid; i < L; i += NT) IDX(a.A, a.lda, b0 + i, jb) = xcol[i];
                 if (hasB)
                     for (int i = tid; i < L; i += NT) IDX(a.B, a.ldb, b0 + i, cB) = ys[i];
             } else {
+                __syncthreads();
                 K1_TICK(2);
                 // ---- (S3) left reflector Q_k^j on A(i1:i2,jb) ----------------------------------
                 if (warp == 0) {
@@ -357,6 +478,7 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
                     }
                 }
                 __syncthreads();
+                K1_TICK(7);
                 const S tau = scal[0];
                 {
                     const S betaS = scal[1];
@@ -366,48 +488,65 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
                     }
                     if (hasB)
                         for (int i = tid; i < t; i += NT) IDX(a.B, a.ldb, b0 + i, cB) = ys[i];
+                    S* qr = a.Qr + ((int64_t)t * K + k) * (r + 1);
+                    for (int c = tid; c < m; c += NT) qr[c] = vq[c];
+                    if (tid == 0) qr[r] = tau;
                 }
-                // ---- (S4) B block <- Q^* B block ---------------------------------------------------
-                if (!is_zero(tau)) {
-                    const S ctau = conjv(tau);
-                    for (int c = warp; c < m; c += NW) {
-                        S s = S(0.0);
-                        for (int i = lane; i < m; i += 32) s += conj_mul(vq[i], Cb[i + c * LDC]);
-                        s = warp_sum(s) * ctau;
-                        for (int i = lane; i < m; i += 32) Cb[i + c * LDC] -= vq[i] * s;
+                __syncthreads();
+                K1_TICK(8);
+                // ---- (S4) B block <- Q^* B block (warps 0..NW/2-1) || T column t (others) ------
+                if (warp < NW / 2) {
+                    if (!is_zero(tau)) {
+                        const S ctau = conjv(tau);
+                        for (int c = warp; c < m; c += NW / 2) {
+                            S s = S(0.0);
+                            for (int i = lane; i < m; i += 32) s += conj_mul(vq[i], Cb[i + c * LDC]);
+                            s = warp_sum(s) * ctau;
+                            for (int i = lane; i < m; i += 32) Cb[i + c * LDC] -= vq[i] * s;
+                        }
+                    }
+                } else {
+                    // xLARFT column t: T(0:t,t) = -tau T(0:t,0:t) (Y(:,0:t)^* v), T(t,t) = tau
+                    const int hn = NT - NT / 2, me = tid - NT / 2;
+                    for (int s = me; s < t; s += hn) {
+                        const S* v = rec + (size_t)s * (r + 1);
+                        const int ms = min(r, n - (j1 + s + k * r));
+                        S d = S(0.0);
+                        for (int ii = t; ii < s + ms && ii - t < m; ++ii) d += conj_mul(v[ii - s], vq[ii - t]);
+                        if (is_zero(v[r])) d = S(0.0);
+                        wu[s] = d;
+                    }
+                    named_bar(2, hn);
+                    S* tr = a.Tr + ((int64_t)t * K + k) * a.TLD;
+                    for (int p = me; p <= t; p += hn) {
+                        S val;
+                        if (p == t) {
+                            val = tau;
+                        } else {
+                            S acc = S(0.0);
+                            for (int s = p; s < t; ++s) acc += Tsm[p * TL + s] * wu[s];
+                            val = -(tau * acc);
+                        }
+                        tr[p] = val;
                     }
                 }
                 __syncthreads();
                 K1_TICK(3);
-                // ---- (S5) RQ on warps [0,NWR) || U_k <- U_k Q_k^j on the other warps --------------
-                if (warp < NWR) {
-                    rq_direction<S, MAXM, NWR>(m, Cb, LDC, bc, uu);
-                    if (NWR == 1) __syncwarp();
-                    else named_bar(1, 32 * NWR);
-                    K1_TICK(6);
-                    if (warp == 0) {
-                        S sig;
-                        double b2;
-                        warp_larfg(m, uu, vz, sig, b2);
-                        if (lane == 0) scal[2] = sig;
-                    }
-                } else if (!is_zero(tau)) {
-                    const int nth = NT - 32 * NWR, me = tid - 32 * NWR;
-                    for (int l = me; l < tm; l += nth) {
-                        S s = S(0.0);
-                        for (int c = 0; c < m; ++c) s = fma_s(Ub[l * LU + t + c], vq[c], s);
-                        s = s * tau;
-                        for (int c = 0; c < m; ++c) {
-                            const S v = Ub[l * LU + t + c] - s * conjv(vq[c]);
-                            Ub[l * LU + t + c] = v;
-                            Uk[(int64_t)l * LDB + t + c] = v;
-                        }
-                    }
+                // ---- (S5) RQ of the block -> Z_k^j ---------------------------------------------
+                if (tid < RQCfg<S, MAXM>::NTHR) rq_direction<S, MAXM>(m, Cb, LDC, ring, &rq_flag, uu);
+                __syncthreads();
+                if (tid == 0) rq_flag = 1 << 30;
+                K1_TICK(6);
+                if (warp == 0) {
+                    S sig;
+                    double b2;
+                    warp_larfg(m, uu, vz, sig, b2);
+                    if (lane == 0) scal[2] = sig;
                 }
                 __syncthreads();
                 K1_TICK(4);
                 const S sig = scal[2];
-                // ---- (S6) right reflector Z_k^j on the band, V_k update, next column --------------
+                // ---- (S6) right reflector Z_k^j on the band, next column ----------------------
                 const int nBb = max(0, i2 - i4 + 1);  // B rows i4..i2 (block rows i1..i2 from Cb)
                 const int bn = b0 + r;                 // first row of the next step's column
                 for (int e = tid; e < nA + nBb; e += NT) {
@@ -452,14 +591,6 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
                         if (c < m) gp[c * ld] = v[c];
                     if (isA && row >= bn) xnext[row - bn] = v[0];  // column jb of step k+1
                 }
-                if (!is_zero(sig)) {
-                    for (int l = tid; l < tm; l += NT) {  // V_k <- V_k Z_k^j
-                        S s = S(0.0);
-                        for (int c = 0; c < m; ++c) s = fma_s(Vb[l * LU + t + c], vz[c], s);
-                        s = s * sig;
-                        for (int c = 0; c < m; ++c) Vk[(int64_t)l * LDB + t + c] = Vb[l * LU + t + c] - s * conjv(vz[c]);
-                    }
-                }
                 S* zr = a.Zr + ((int64_t)t * K + k) * (r + 1);
                 for (int c = tid; c < m; c += NT) zr[c] = vz[c];
                 if (tid == 0) zr[r] = sig;
@@ -480,6 +611,6 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
         cur ^= 1;
     }
     if (a.prof && tid == 0)
-        for (int i = 0; i < 8; ++i) atomicAdd((unsigned long long*)&a.prof[i], (unsigned long long)pt[i]);
+        for (int i = 0; i < 12; ++i) atomicAdd((unsigned long long*)&a.prof[i], (unsigned long long)pt[i]);
 #undef K1_TICK
 }

@@ -14,6 +14,7 @@
 #include "../../include/ht_stage2.h"
 #include "chase.cuh"
 #include "chain.cuh"
+#include "accum.cuh"
 #include "misc.cuh"
 #include "scalar.cuh"
 
@@ -88,19 +89,19 @@ size_t chain_bytes_rt(int WP, int r, int q) {
     }
 }
 
-// K1 instantiation for the reflector length: the RQ keeps [B_blk; P] in registers on NWR warps
+// K1 instantiation for the reflector length (the RQ keeps [C; P] rows in registers)
 template <typename S>
 const void* chase_kernel_for(int r) {
+    if (r <= 8) return (const void*)chase_kernel<S, CHASE_NT, 8>;
+    if (r <= 16) return (const void*)chase_kernel<S, CHASE_NT, 16>;
+    if (r <= 32) return (const void*)chase_kernel<S, CHASE_NT, 32>;
     if constexpr (sizeof(S) == 8) {
-        if (r <= 16) return (const void*)chase_kernel<S, CHASE_NT, 16, 1>;
-        if (r <= 32) return (const void*)chase_kernel<S, CHASE_NT, 32, 1>;
-        if (r <= 64) return (const void*)chase_kernel<S, CHASE_NT, 64, 4>;
-    } else {
-        if (r <= 16) return (const void*)chase_kernel<S, CHASE_NT, 16, 1>;
-        if (r <= 32) return (const void*)chase_kernel<S, CHASE_NT, 32, 2>;
+        if (r <= 64) return (const void*)chase_kernel<S, CHASE_NT, 64>;
     }
     return nullptr;
 }
+
+constexpr int ACC_NT = 256;
 
 template <typename S>
 int run(int64_t n64, int64_t r64, S* H, int64_t ldh, S* T, int64_t ldt, S* Q, int64_t ldq, S* Z,
@@ -159,10 +160,11 @@ int run(int64_t n64, int64_t r64, S* H, int64_t ldh, S* T, int64_t ldt, S* Q, in
     const int LDB = chain_ldb(WP);
     const int Kmax = 1 + (n - 1 - 2) / r;
     const int chase_budget = 200 * 1024;
-    const size_t chase_base = chase_smem_elems<S>(r, w, 0) * sizeof(S);
+    const size_t chase_base = chase_smem_elems<S>(r, q, 0) * sizeof(S);
     const int strip_cap = (int)std::max<int64_t>(0, ((int64_t)chase_budget - (int64_t)chase_base) /
                                                         (int64_t)((r + 1) * sizeof(S)));
-    const size_t chase_bytes = chase_smem_elems<S>(r, w, strip_cap) * sizeof(S);
+    const size_t chase_bytes = chase_smem_elems<S>(r, q, strip_cap) * sizeof(S);
+    const size_t acc_bytes = accum_smem_bytes<S>(r, q);
     const void* chase_fn = chase_kernel_for<S>(r);
     if (!chase_fn || q > 148) return HT_EUNSUPPORTED;  // one co-resident CTA per sweep
     const size_t ch_bytes = chain_bytes_rt<S>(WP, r, q);
@@ -170,22 +172,29 @@ int run(int64_t n64, int64_t r64, S* H, int64_t ldh, S* T, int64_t ldt, S* Q, in
     CK(cudaGetDevice(&dev));
     CK(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
     CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-    if (chase_bytes > (size_t)smem_optin || ch_bytes > (size_t)smem_optin) return HT_EUNSUPPORTED;
+    if (chase_bytes > (size_t)smem_optin || ch_bytes > (size_t)smem_optin || acc_bytes > (size_t)smem_optin)
+        return HT_EUNSUPPORTED;
     CK(cudaFuncSetAttribute(chase_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)chase_bytes));
+    CK(cudaFuncSetAttribute(accum_kernel<S, ACC_NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)acc_bytes));
 
     // ---- workspace (stream-ordered) ----
-    S *U = nullptr, *V = nullptr, *Zr = nullptr;
+    S *U = nullptr, *V = nullptr, *Zr = nullptr, *Qr = nullptr, *Tr = nullptr;
     int* prog = nullptr;
     const size_t blk_elems = (size_t)Kmax * WP * LDB;
+    const size_t rec_elems = (size_t)q * Kmax * (r + 1);
+    const int TLD = q;
+    const size_t t_elems = (size_t)q * Kmax * TLD;
     CK(cudaMallocAsync(&U, blk_elems * sizeof(S), stream));
     CK(cudaMallocAsync(&V, blk_elems * sizeof(S), stream));
-    CK(cudaMallocAsync(&Zr, (size_t)q * Kmax * (r + 1) * sizeof(S), stream));
+    CK(cudaMallocAsync(&Zr, rec_elems * sizeof(S), stream));
+    CK(cudaMallocAsync(&Qr, rec_elems * sizeof(S), stream));
+    CK(cudaMallocAsync(&Tr, t_elems * sizeof(S), stream));
     CK(cudaMallocAsync(&prog, (size_t)q * sizeof(int), stream));
     long long* k1prof = nullptr;  // HT_K1PROF=1: chase phase cycle counts (stderr)
     const bool k1p = getenv("HT_K1PROF") != nullptr;
     if (k1p) {
-        CK(cudaMallocAsync(&k1prof, 8 * sizeof(long long), stream));
-        CK(cudaMemsetAsync(k1prof, 0, 8 * sizeof(long long), stream));
+        CK(cudaMallocAsync(&k1prof, 12 * sizeof(long long), stream));
+        CK(cudaMemsetAsync(k1prof, 0, 12 * sizeof(long long), stream));
     }
 
     // kernel-class timing: 4 events per group from a pool, summed after one sync at the end
@@ -201,12 +210,14 @@ int run(int64_t n64, int64_t r64, S* H, int64_t ldh, S* T, int64_t ldt, S* Q, in
         const int qp = std::min(q, n - 1 - j1);
         const int K = 1 + (n - j1 - 2) / r;
         if (prof) CK(cudaEventRecord(ev[4 * g + 0], stream));
-        init_blocks_kernel<S><<<std::min<int64_t>(4 * nsm, ((int64_t)K * WP * LDB + 255) / 256), 256, 0,
-                                stream>>>(U, V, K, WP, LDB, n, j1, qp + r - 1, r);
         CK(cudaMemsetAsync(prog, 0, (size_t)q * sizeof(int), stream));
-        ChaseArgs<S> ca{n, r, qp, j1, K, WP, LDB, H, ldh, T, ldt, U, V, Zr, prog, strip_cap, k1prof};
+        CK(cudaMemsetAsync(Qr, 0, (size_t)qp * K * (r + 1) * sizeof(S), stream));
+        CK(cudaMemsetAsync(Zr, 0, (size_t)qp * K * (r + 1) * sizeof(S), stream));
+        ChaseArgs<S> ca{n, r, qp, j1, K, H, ldh, T, ldt, Qr, Zr, Tr, TLD, prog, strip_cap, k1prof};
         void* kargs[] = {&ca};
         CK(cudaLaunchCooperativeKernel(chase_fn, dim3(qp), dim3(CHASE_NT), kargs, chase_bytes, stream));
+        AccumArgs<S> aa{n, r, qp, j1, K, WP, LDB, Qr, Zr, U, V};
+        accum_kernel<S, ACC_NT><<<dim3(K, 2), ACC_NT, acc_bytes, stream>>>(aa);
         g_last_launches += 2;
         if (prof) CK(cudaEventRecord(ev[4 * g + 1], stream));
         // ---- apply phase: right updates of H, T (staircase + V_k), then left (U_k^*) ----
@@ -234,16 +245,18 @@ int run(int64_t n64, int64_t r64, S* H, int64_t ldh, S* T, int64_t ldt, S* Q, in
     CK(cudaFreeAsync(U, stream));
     CK(cudaFreeAsync(V, stream));
     CK(cudaFreeAsync(Zr, stream));
+    CK(cudaFreeAsync(Qr, stream));
+    CK(cudaFreeAsync(Tr, stream));
     CK(cudaFreeAsync(prog, stream));
     if (k1p) {
-        long long h[8];
+        long long h[12];
         CK(cudaMemcpyAsync(h, k1prof, sizeof(h), cudaMemcpyDeviceToHost, stream));
         CK(cudaStreamSynchronize(stream));
-        const char* nm[8] = {"wait", "loads", "catchup", "larfg+QB", "RQ||U", "strip+V", "RQonly", "loop"};
+        const char* nm[12] = {"wait", "loads", "catchup", "QB+T", "larfgZ", "strip", "RQ", "larfgQ", "writes", "s9", "s10", "s11"};
         double tot = 0;
         for (long long x : h) tot += (double)x;
         fprintf(stderr, "K1 cycles (sum over CTAs):");
-        for (int i = 0; i < 8; ++i) fprintf(stderr, " %s=%.1f%%", nm[i], 100.0 * h[i] / tot);
+        for (int i = 0; i < 12; ++i) fprintf(stderr, " %s=%.1f%%", nm[i], 100.0 * h[i] / tot);
         fprintf(stderr, " total=%.3g\n", tot);
         CK(cudaFreeAsync(k1prof, stream));
     }

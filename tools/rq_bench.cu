@@ -1,36 +1,57 @@
-// dev micro-benchmark: cycles of the K1 RQ direction routine on one warp (not product code)
+// dev micro-benchmark (not product code): cycles of K1 pieces on one CTA of 256 threads
 #include <cstdio>
 #include <cstdlib>
+#include <cmath>
 #include "../paper_2301_07964_b200/csrc/chase.cuh"
 
-template <int MAXM, int NWR>
+template <int MAXM>
 __global__ void bench(const double* C0, double* out, long long* cyc, int m, int reps) {
-    __shared__ double Cb[64 * 65];
-    __shared__ double bc[2 * 80];
+    extern __shared__ double dyn[];
+    double* Cb = dyn;
+    double* piv = dyn + 64 * 65;
+    __shared__ int flag;
+    if (threadIdx.x == 0) flag = 1 << 30;
+    __syncthreads();
     __shared__ double uu[80];
     for (int e = threadIdx.x; e < m * m; e += blockDim.x) Cb[(e % m) + (e / m) * (m + 1)] = C0[e];
     __syncthreads();
     long long t0 = clock64();
     for (int it = 0; it < reps; ++it) {
-        if (threadIdx.x < 32 * NWR) rq_direction<double, MAXM, NWR>(m, Cb, m + 1, bc, uu);
+        if (threadIdx.x < RQCfg<double, MAXM>::NTHR) rq_direction<double, MAXM>(m, Cb, m + 1, piv, &flag, uu);
+        __syncthreads();
+        if (threadIdx.x == 0) flag = 1 << 30;
         __syncthreads();
     }
     long long t1 = clock64();
     if (threadIdx.x < m) out[threadIdx.x] = uu[threadIdx.x];
-    if (threadIdx.x == 0) cyc[0] = (t1 - t0) / reps;
+    __syncthreads();
+    double tau; double beta;
+    for (int it = 0; it < reps; ++it) {
+        if (threadIdx.x < 32) warp_larfg(m, uu, piv, tau, beta);
+        __syncthreads();
+    }
+    long long t2 = clock64();
+    
+    if (threadIdx.x == 0) { cyc[0] = (t1 - t0) / reps; cyc[1] = (t2 - t1) / reps; }
 }
 
 int main() {
-    int ms[3] = {16, 32, 64};
-    for (int mi = 0; mi < 3; ++mi) {
+    int ms[4] = {8, 16, 32, 64};
+    for (int mi = 0; mi < 4; ++mi) {
         int m = ms[mi];
         double *C, *out; long long* cyc;
-        cudaMallocManaged(&C, m * m * 8); cudaMallocManaged(&out, 64 * 8); cudaMallocManaged(&cyc, 8);
+        cudaMallocManaged(&C, m * m * 8); cudaMallocManaged(&out, 64 * 8); cudaMallocManaged(&cyc, 16);
         for (int i = 0; i < m * m; ++i) C[i] = (rand() / (double)RAND_MAX) - 0.5;
-        if (m == 16) bench<16, 1><<<1, 256>>>(C, out, cyc, m, 20);
-        if (m == 32) bench<32, 1><<<1, 256>>>(C, out, cyc, m, 20);
-        if (m == 64) bench<64, 4><<<1, 256>>>(C, out, cyc, m, 20);
+        if (m == 8) { cudaFuncSetAttribute(bench<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100000); bench<8><<<1, 256, 100000>>>(C, out, cyc, m, 20); }
+        if (m == 16) { cudaFuncSetAttribute(bench<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100000); bench<16><<<1, 256, 100000>>>(C, out, cyc, m, 20); }
+        if (m == 32) { cudaFuncSetAttribute(bench<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100000); bench<32><<<1, 256, 100000>>>(C, out, cyc, m, 20); }
+        if (m == 64) { cudaFuncSetAttribute(bench<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100000); bench<64><<<1, 256, 100000>>>(C, out, cyc, m, 20); }
         cudaDeviceSynchronize();
-        printf("m=%d cycles/RQ=%lld (%s) u0=%g\n", m, cyc[0], cudaGetErrorString(cudaGetLastError()), out[0]);
+        // residual of rows 1..m-1 of C u (must vanish) and |u|
+        double res = 0, nu = 0, nc = 0;
+        for (int i = 0; i < m; ++i) nu += out[i] * out[i];
+        for (int i = 1; i < m; ++i) { double s = 0; for (int c = 0; c < m; ++c) s += C[i + c * m] * out[c]; res += s * s; }
+        for (int i = 0; i < m * m; ++i) nc += C[i] * C[i];
+        printf("m=%d cycles/RQ=%lld larfg=%lld (%s) |u|=%.15f res=%.3e\n", m, cyc[0], cyc[1], cudaGetErrorString(cudaGetLastError()), sqrt(nu), sqrt(res / nc));
     }
 }
