@@ -44,13 +44,15 @@ struct ChainParams {
     const S* Zr;  // staircase reflectors: (qp*K) records of (r+1)
 };
 
-constexpr int CH_BM = 64;      // tile rows per CTA
-constexpr int CH_NT = 256;     // 8 warps: 2 (rows) x 4 (cols)
+constexpr int CH_BM = 32;      // tile rows per CTA (one warp row of 4 m8 tiles)
 constexpr int CH_KC = 16;      // k rows per ring chunk
 constexpr int CH_STAGES = 3;   // ring depth
 constexpr int CH_LDX = CH_BM + 8;  // smem column stride of X (== 8 mod 16: conflict-free)
 
 __host__ __device__ constexpr int chain_ldb(int WP) { return WP + 8; }
+// warps along the window's columns: each warp owns WP/WN columns (a multiple of 8)
+__host__ __device__ constexpr int chain_wn(int WP) { return (WP % 64 == 0) ? 8 : 4; }
+__host__ __device__ constexpr int chain_nt(int WP) { return 32 * chain_wn(WP); }
 
 // dynamic smem: [64 B mbarriers][circular X: (w+r) x CH_LDX][block ring][staircase refl.]
 template <typename S, int WP>
@@ -140,18 +142,23 @@ __device__ __forceinline__ S maybe_conj(S x, bool c) {
 }
 
 // ---------------------------------------------------------------------------------------
+// One tile's descending-k chain.  Returns true if it initialised (and so must invalidate) the
+// ring's mbarriers.
 template <typename S, int WP>
-__global__ void __launch_bounds__(CH_NT) chain_kernel(ChainParams<S> P) {
-    extern __shared__ __align__(16) unsigned char smraw[];
+__device__ __forceinline__ bool chain_tile(const ChainParams<S>& P, int bid, unsigned char* smraw) {
     constexpr int LDB = chain_ldb(WP);
-    constexpr int MT = 4;            // 8-row tiles per warp (32 rows)
-    constexpr int NTL = WP / 32;     // 8-col tiles per warp (WP/4 cols)
+    constexpr int CH_NT = chain_nt(WP);
+    constexpr int NW = CH_NT / 32;
+    constexpr int WN = chain_wn(WP);
+    constexpr int MT = CH_BM / 8;    // 8-row tiles per warp (all CH_BM rows)
+    constexpr int NTL = WP / (8 * WN);  // 8-col tiles per warp
+    static_assert(WP % (8 * WN) == 0, "window padding");
     const int n = P.n, r = P.r, qp = P.qp, j1 = P.j1, K = P.K;
     const int w = qp + r - 1;
     const int CIRC = w + r;  // circular buffer columns
 
     // ---- which job / tile ----
-    int bid = blockIdx.x, jb_ = 0;
+    int jb_ = 0;
     if (P.njobs > 1 && bid >= P.job[0].ntiles) {
         bid -= P.job[0].ntiles;
         jb_ = 1;
@@ -160,7 +167,7 @@ __global__ void __launch_bounds__(CH_NT) chain_kernel(ChainParams<S> P) {
     const int mode = J.mode;
     const bool trans = J.trans != 0;
     const int R0 = bid * CH_BM + 1;  // first tile row (1-based)
-    if (R0 > n) return;
+    if (R0 > n) return false;
     const int nr = min(CH_BM, n - R0 + 1);
     const int R1 = R0 + nr - 1;
 
@@ -178,14 +185,14 @@ __global__ void __launch_bounds__(CH_NT) chain_kernel(ChainParams<S> P) {
     };
     int kstart = K - 1, kend = 0;
     if (mode == CM_AB_RIGHT) {
-        if (rowmax(K - 1) < R0) return;
+        if (rowmax(K - 1) < R0) return false;
         while (kend < K - 1 && rowmax(kend) < R0) ++kend;
     } else if (mode == CM_A_LEFT || mode == CM_B_LEFT) {
         while (kstart >= 0 && cstart(kstart) >= R1) --kstart;
-        if (kstart < 0) return;
+        if (kstart < 0) return false;
     }
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int wm = warp & 1, wn = warp >> 1;
+    const int wn = warp;
 
     // zero the circular buffer (padded K rows of the blocks are zero; keep X finite)
     for (int e = tid; e < CIRC * CH_LDX; e += CH_NT) X[e] = S(0.0);
@@ -200,38 +207,37 @@ __global__ void __launch_bounds__(CH_NT) chain_kernel(ChainParams<S> P) {
         return trans ? &IDX(J.M, J.ld, c, g) : &IDX(J.M, J.ld, g, c);
     };
     // load chain indices [c0, c0+cnt) into circular positions starting at p (cp.async)
+    // (lanes run along the contiguous direction of the global matrix; no integer division)
     auto load_cols = [&](int c0, int cnt, int p) {
         if (!trans) {
-            for (int e = tid; e < cnt * nr; e += CH_NT) {
-                const int i = e % nr, l = e / nr;
+            for (int l = warp; l < cnt; l += NW) {
                 int pos = p + l;
                 if (pos >= CIRC) pos -= CIRC;
-                cp_async_elem(&X[pos * CH_LDX + i], gptr(R0 + i, c0 + l));
+                for (int i = lane; i < nr; i += 32) cp_async_elem(&X[pos * CH_LDX + i], gptr(R0 + i, c0 + l));
             }
         } else {
-            for (int e = tid; e < cnt * nr; e += CH_NT) {
-                const int l = e % cnt, i = e / cnt;
-                int pos = p + l;
-                if (pos >= CIRC) pos -= CIRC;
-                cp_async_elem(&X[pos * CH_LDX + i], gptr(R0 + i, c0 + l));
-            }
+            for (int i = warp; i < nr; i += NW)
+                for (int l = lane; l < cnt; l += 32) {
+                    int pos = p + l;
+                    if (pos >= CIRC) pos -= CIRC;
+                    cp_async_elem(&X[pos * CH_LDX + i], gptr(R0 + i, c0 + l));
+                }
         }
     };
     auto store_cols = [&](int c0, int cnt, int p) {
         if (!trans) {
-            for (int e = tid; e < cnt * nr; e += CH_NT) {
-                const int i = e % nr, l = e / nr;
+            for (int l = warp; l < cnt; l += NW) {
                 int pos = p + l;
                 if (pos >= CIRC) pos -= CIRC;
-                *gptr(R0 + i, c0 + l) = X[pos * CH_LDX + i];
+                for (int i = lane; i < nr; i += 32) *gptr(R0 + i, c0 + l) = X[pos * CH_LDX + i];
             }
         } else {
-            for (int e = tid; e < cnt * nr; e += CH_NT) {
-                const int l = e % cnt, i = e / cnt;
-                int pos = p + l;
-                if (pos >= CIRC) pos -= CIRC;
-                *gptr(R0 + i, c0 + l) = X[pos * CH_LDX + i];
-            }
+            for (int i = warp; i < nr; i += NW)
+                for (int l = lane; l < cnt; l += 32) {
+                    int pos = p + l;
+                    if (pos >= CIRC) pos -= CIRC;
+                    *gptr(R0 + i, c0 + l) = X[pos * CH_LDX + i];
+                }
         }
     };
 
@@ -281,10 +287,9 @@ __global__ void __launch_bounds__(CH_NT) chain_kernel(ChainParams<S> P) {
         const bool stair = mode == CM_AB_RIGHT && qp >= 2 && max(i5s, R0) <= min(rowmax(k), R1);
         if (stair) {
             const S* src = P.Zr + (size_t)k * (r + 1);
-            for (int e = tid; e < (qp - 1) * (r + 1); e += CH_NT) {
-                const int t = 1 + e / (r + 1), c = e % (r + 1);
-                cp_async_elem(&zsm[(size_t)t * (r + 1) + c], src + (size_t)t * K * (r + 1) + c);
-            }
+            for (int t = 1 + warp; t < qp; t += NW)
+                for (int c = lane; c <= r; c += 32)
+                    cp_async_elem(&zsm[(size_t)t * (r + 1) + c], src + (size_t)t * K * (r + 1) + c);
         }
         cp_async_commit();
 
@@ -295,8 +300,8 @@ __global__ void __launch_bounds__(CH_NT) chain_kernel(ChainParams<S> P) {
 #pragma unroll
             for (int nt = 0; nt < NTL; ++nt) acc_zero(acc[mt][nt]);
         const int nch = (wk + CH_KC - 1) / CH_KC;
-        const int rowb = wm * 32 + (lane >> 2);
-        const int colb = wn * (WP / 4) + (lane >> 2);
+        const int rowb = lane >> 2;
+        const int colb = wn * (WP / WN) + (lane >> 2);
         for (int ch = 0; ch < nch; ++ch) {
             const int s = cseq % CH_STAGES;
             mbar_wait(&bars[s], (cseq / CH_STAGES) & 1);
@@ -335,7 +340,7 @@ __global__ void __launch_bounds__(CH_NT) chain_kernel(ChainParams<S> P) {
             for (int nt = 0; nt < NTL; ++nt)
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
-                    const int col = wn * (WP / 4) + nt * 8 + (lane & 3) * 2 + h;
+                    const int col = wn * (WP / WN) + nt * 8 + (lane & 3) * 2 + h;
                     if (upd && col < wk) {
                         int pos = p + col;
                         if (pos >= CIRC) pos -= CIRC;
@@ -346,7 +351,7 @@ __global__ void __launch_bounds__(CH_NT) chain_kernel(ChainParams<S> P) {
         if (stair) {  // Alg. 4 lines 4-9: rows i5s..i4(k,j) get Z_k^j one by one, j ascending
             cp_async_wait_all();
             __syncthreads();
-            const int row = tid >> 2, part = tid & 3;  // 4 threads per row
+            const int row = tid >> 2, part = tid & 3;  // 4 threads per row (CH_NT/4 >= CH_BM)
             const int g = R0 + row;
             const bool active = row < nr && g >= i5s && g <= rowmax(k);
             for (int t = 1; t < qp; ++t) {
@@ -388,4 +393,23 @@ __global__ void __launch_bounds__(CH_NT) chain_kernel(ChainParams<S> P) {
         if (p < 0) p += CIRC;
     }
     cp_async_wait_all();
+    return true;
 }
+
+// Persistent over tiles: CTA b processes tiles b, b + gridDim.x, ... (a grid smaller than the
+// tile count leaves SMs free for the chase kernel running concurrently on another stream).
+template <typename S, int WP>
+__global__ void __launch_bounds__(chain_nt(WP)) chain_kernel(ChainParams<S> P) {
+    extern __shared__ __align__(16) unsigned char smraw[];
+    const int total = P.job[0].ntiles + (P.njobs > 1 ? P.job[1].ntiles : 0);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smraw);
+    for (int b = blockIdx.x; b < total; b += gridDim.x) {
+        const bool used = chain_tile<S, WP>(P, b, smraw);
+        __syncthreads();
+        if (used && threadIdx.x == 0)
+            for (int s = 0; s < CH_STAGES; ++s)
+                asm volatile("mbarrier.inval.shared::cta.b64 [%0];\n" ::"r"(smem_u32(&bars[s])) : "memory");
+        __syncthreads();
+    }
+}
+

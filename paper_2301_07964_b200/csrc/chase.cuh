@@ -34,7 +34,7 @@ struct ChaseArgs {
     S* Zr;      // (qp*K) records of (r+1): v of Z_k^j, sigma at [r]
     S* Tr;      // (qp*K) records of TLD: column t of window k's WY factor T (rows 0..t)
     int TLD;
-    int* prog;  // qp counters: steps completed by each sweep of the group
+    int* prog;  // qp counters: steps completed by each sweep of the group; prog[qp] = sweep ticket
     int strip_cap;  // strip rows (A then B) staged in shared memory per step
     long long* prof;  // optional: per-CTA cycle counts of the step phases (8 slots)
 };
@@ -285,6 +285,127 @@ __device__ __forceinline__ void rq_direction(int m, const S* Cb, int LDC, S* rin
     }
 }
 
+// Fully unrolled variant for MAXM <= 32 (the common r <= 32 case): one thread per row (group A =
+// warp 0 holds C, group B = warp 1 holds P), the stage index i is a compile-time constant in
+// every unrolled copy, so column masks and the pick of row[i] cost nothing; scalars use the
+// MUFU-seeded rsqrt / reciprocal (fast_rsqrt, fast_rcp).  Same mathematics as rq_direction.
+template <typename S, int MAXM>
+__device__ __forceinline__ void rq_direction_u(int m, const S* Cb, int LDC, S* ring, volatile int* flag, S* uu) {
+    constexpr int PL = MAXM + 4;
+    const int tid = threadIdx.x;
+    const bool grpB = tid >= 32;
+    const int l = tid & 31;
+    const bool live = l < m && l < MAXM;
+    S row[MAXM];
+#pragma unroll
+    for (int c = 0; c < MAXM; ++c) {
+        S v = S(0.0);
+        if (live && c < m) v = grpB ? S(l == c ? 1.0 : 0.0) : Cb[l + c * LDC];
+        row[c] = v;
+    }
+    if (!grpB) {
+        if (live && l == m - 1) {
+#pragma unroll
+            for (int c = 0; c < MAXM; ++c) ring[(size_t)(m - 1) * PL + c] = row[c];
+        }
+        __syncwarp();
+#pragma unroll
+        for (int i = MAXM - 1; i >= 1; --i) {
+            if (i <= m - 1) {  // uniform
+                const S* pv = ring + (size_t)i * PL;
+                const S alpha = conjv(pv[i]);
+                double n4[4] = {0.0, 0.0, 0.0, 0.0};
+                S g4[4] = {S(0.0), S(0.0), S(0.0), S(0.0)};
+#pragma unroll
+                for (int c = 0; c < i; ++c) {
+                    const S b = pv[c];
+                    n4[c & 3] += abs2(b);
+                    g4[c & 3] = fma_s(row[c], conjv(b), g4[c & 3]);
+                }
+                const double nx = (n4[0] + n4[1]) + (n4[2] + n4[3]);
+                const S g = (g4[0] + g4[1]) + (g4[2] + g4[3]);
+                S K1 = S(0.0), K2 = S(0.0);
+                if (!(nx == 0.0 && im(alpha) == 0.0)) {
+                    const double s2 = abs2(alpha) + nx;
+                    const double y = fast_rsqrt(s2);
+                    const double nrm = s2 * y;
+                    const double beta = (re(alpha) >= 0.0) ? -nrm : nrm;
+                    K2 = alpha - S(beta);
+                    if constexpr (sizeof(S) == 8) {
+                        K1 = S(fast_rcp(s2 + fabs(re(alpha)) * nrm));
+                    } else {
+                        const S tau = (S(beta) - alpha) * ((re(alpha) >= 0.0) ? -y : y);  // 1/beta
+                        K1 = tau * fast_rcp(abs2(K2));
+                    }
+                }
+                S f = K1 * (g + K2 * row[i]);
+                if (!(live && l < i)) f = S(0.0);
+#pragma unroll
+                for (int c = 0; c < i; ++c) row[c] -= f * pv[c];
+                if (l == 0) {
+                    ring[(size_t)i * PL + MAXM] = K1;
+                    ring[(size_t)i * PL + MAXM + 1] = K2;
+                }
+                if (live && l == i - 1) {
+#pragma unroll
+                    for (int c = 0; c < i; ++c) ring[(size_t)(i - 1) * PL + c] = row[c];
+                }
+                __syncwarp();
+                if (l == 0) st_release_cta(flag, i);
+            }
+        }
+        if constexpr (sizeof(S) != 8) {
+            const S alpha = conjv(ring[0]);
+            S tau = S(0.0);
+            if (im(alpha) != 0.0) {
+                const double nrm = sqrt(abs2(alpha));
+                const double beta = (re(alpha) >= 0.0) ? -nrm : nrm;
+                tau = (S(beta) - alpha) * (1.0 / beta);
+            }
+            if (l == 0) {
+                ring[MAXM] = tau;
+                st_release_cta(flag, 0);
+            }
+        }
+    } else {
+        constexpr int ILAST = (sizeof(S) == 8) ? 1 : 0;
+#pragma unroll
+        for (int i = MAXM - 1; i >= ILAST; --i) {
+            if (i <= m - 1) {
+                while (ld_acquire_cta(flag) > i) {
+                }
+                const S* pv = ring + (size_t)i * PL;
+                const S K1 = pv[MAXM];
+                if (i == 0) {
+                    if (live) row[0] -= K1 * row[0];
+                } else {
+                    const S K2 = pv[MAXM + 1];
+                    S g4[4] = {S(0.0), S(0.0), S(0.0), S(0.0)};
+#pragma unroll
+                    for (int c = 0; c < i; ++c) g4[c & 3] = fma_s(row[c], conjv(pv[c]), g4[c & 3]);
+                    const S g = (g4[0] + g4[1]) + (g4[2] + g4[3]);
+                    S f = K1 * (g + K2 * row[i]);
+                    if (!live) f = S(0.0);
+#pragma unroll
+                    for (int c = 0; c < i; ++c) row[c] -= f * pv[c];
+                }
+            }
+        }
+        if (live) uu[l] = row[0];
+    }
+}
+
+template <typename S, int MAXM>
+__host__ __device__ constexpr bool rq_unrolled() { return MAXM * (int)sizeof(S) <= 256; }  // real <= 32, complex <= 16
+template <typename S, int MAXM>
+__host__ __device__ constexpr int rq_nthr() { return rq_unrolled<S, MAXM>() ? 64 : RQCfg<S, MAXM>::NTHR; }
+
+template <typename S, int MAXM>
+__device__ __forceinline__ void rq_dir(int m, const S* Cb, int LDC, S* ring, volatile int* flag, S* uu) {
+    if constexpr (rq_unrolled<S, MAXM>()) rq_direction_u<S, MAXM>(m, Cb, LDC, ring, flag, uu);
+    else rq_direction<S, MAXM>(m, Cb, LDC, ring, flag, uu);
+}
+
 template <typename S>
 __host__ __device__ inline size_t chase_smem_elems(int r, int qp, int strip_cap) {
     const int w = qp + r - 1;
@@ -330,7 +451,12 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
     S* wu = zy + (qp + 8);                // Y^* v (T column build)
     S* strip = wu + (qp + 8);  // strip_cap rows x (r+1) (row-major)
     const int LDC = r + 1;
-    const int t = blockIdx.x;
+    // sweep index by ticket (not blockIdx): a CTA only ever waits on a sweep whose CTA already
+    // started, so a normal (non-cooperative) launch cannot deadlock when SMs are shared
+    __shared__ int t_sh;
+    if (threadIdx.x == 0) t_sh = atomicAdd(&a.prog[qp], 1);
+    __syncthreads();
+    const int t = t_sh;
     if (t >= qp) return;
     const int j = j1 + t;
     const int kcount = min(K, 2 + (n - j - 1) / r);
@@ -533,7 +659,7 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
                 __syncthreads();
                 K1_TICK(3);
                 // ---- (S5) RQ of the block -> Z_k^j ---------------------------------------------
-                if (tid < RQCfg<S, MAXM>::NTHR) rq_direction<S, MAXM>(m, Cb, LDC, ring, &rq_flag, uu);
+                if (tid < rq_nthr<S, MAXM>()) rq_dir<S, MAXM>(m, Cb, LDC, ring, &rq_flag, uu);
                 __syncthreads();
                 if (tid == 0) rq_flag = 1 << 30;
                 K1_TICK(6);

@@ -53,28 +53,45 @@ template <typename S, int WP>
 size_t chain_bytes(int r, int q) { return chain_smem_bytes<S, WP>(r, q); }
 
 template <typename S, int WP>
-int launch_chain(const ChainParams<S>& P, int grid, int r, int q, cudaStream_t st) {
-    const size_t bytes = chain_bytes<S, WP>(r, q);
+int launch_chain(const ChainParams<S>& P, int grid, int r, int q, cudaStream_t st, size_t min_smem) {
+    const size_t bytes = std::max(chain_bytes<S, WP>(r, q), min_smem);
     static bool attr_set = false;  // per instantiation
     if (!attr_set) {
         CK(cudaFuncSetAttribute(chain_kernel<S, WP>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
         attr_set = true;
     }
-    chain_kernel<S, WP><<<grid, CH_NT, bytes, st>>>(P);
+    chain_kernel<S, WP><<<grid, chain_nt(WP), bytes, st>>>(P);
     CK(cudaGetLastError());
     return HT_OK;
 }
 
+// min_smem > 0 pads the dynamic shared memory so that at most one CTA fits per SM (used by the
+// side-stream Q/Z chains: a grid of nsm - q such CTAs leaves q whole SMs for the next chase).
 template <typename S>
-int chain(const ChainParams<S>& P, int WP, int grid, int r, int q, cudaStream_t st) {
+int chain(const ChainParams<S>& P, int WP, int grid, int r, int q, cudaStream_t st, size_t min_smem = 0) {
     switch (WP) {
-        case 32: return launch_chain<S, 32>(P, grid, r, q, st);
-        case 64: return launch_chain<S, 64>(P, grid, r, q, st);
-        case 96: return launch_chain<S, 96>(P, grid, r, q, st);
-        case 128: return launch_chain<S, 128>(P, grid, r, q, st);
-        case 160: return launch_chain<S, 160>(P, grid, r, q, st);
+        case 32: return launch_chain<S, 32>(P, grid, r, q, st, min_smem);
+        case 64: return launch_chain<S, 64>(P, grid, r, q, st, min_smem);
+        case 96: return launch_chain<S, 96>(P, grid, r, q, st, min_smem);
+        case 128: return launch_chain<S, 128>(P, grid, r, q, st, min_smem);
+        case 160: return launch_chain<S, 160>(P, grid, r, q, st, min_smem);
         default: return HT_EUNSUPPORTED;
     }
+}
+
+template <typename S>
+int chain_prepare(int WP) {  // smem attribute outside any stream capture
+    ChainParams<S> dummy{};
+    (void)dummy;
+    switch (WP) {
+        case 32: CK(cudaFuncSetAttribute(chain_kernel<S, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024)); break;
+        case 64: CK(cudaFuncSetAttribute(chain_kernel<S, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024)); break;
+        case 96: CK(cudaFuncSetAttribute(chain_kernel<S, 96>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024)); break;
+        case 128: CK(cudaFuncSetAttribute(chain_kernel<S, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024)); break;
+        case 160: CK(cudaFuncSetAttribute(chain_kernel<S, 160>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024)); break;
+        default: return HT_EUNSUPPORTED;
+    }
+    return HT_OK;
 }
 
 template <typename S>
@@ -102,6 +119,254 @@ const void* chase_kernel_for(int r) {
 }
 
 constexpr int ACC_NT = 256;
+
+template <typename S>
+struct Plan {
+    int n, r, q, WP, LDB, Kmax, strip_cap;
+    size_t chase_bytes, acc_bytes;
+    const void* chase_fn;
+    S* H;
+    int64_t ldh;
+    S* T;
+    int64_t ldt;
+    S* Q;
+    int64_t ldq;
+    S* Z;
+    int64_t ldz;
+    int qz_ctas;
+    bool qz() const { return Q || Z; }
+    bool same(const Plan& o) const {
+        return n == o.n && r == o.r && q == o.q && strip_cap == o.strip_cap && H == o.H && ldh == o.ldh &&
+               T == o.T && ldt == o.ldt && Q == o.Q && ldq == o.ldq && Z == o.Z && ldz == o.ldz;
+    }
+};
+
+// Workspace of one reduction: NUV U/V buffers (the Q/Z chains of group g run on the side
+// stream while later groups are chased; the side stream may lag NUV-1 groups), reflector
+// records, WY factors, progress counters.
+constexpr int NUV = 4;
+template <typename S>
+struct Workspace {
+    S *U[NUV] = {}, *V[NUV] = {}, *Zr = nullptr, *Qr = nullptr, *Tr = nullptr;
+    int* prog = nullptr;
+    long long* k1prof = nullptr;
+    long long k1prof_host[12] = {0};
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_uv[NUV] = {}, ev_qz[NUV] = {};
+    bool async = true;
+
+    int alloc(const Plan<S>& p, cudaStream_t stream, bool async_, bool k1p) {
+        async = async_;
+        const size_t blk = (size_t)p.Kmax * p.WP * p.LDB * sizeof(S);
+        const size_t rec = (size_t)p.q * p.Kmax * (p.r + 1) * sizeof(S);
+        const size_t tf = (size_t)p.q * p.Kmax * p.q * sizeof(S);
+        auto mal = [&](void** ptr, size_t bytes) -> cudaError_t {
+            return async ? cudaMallocAsync(ptr, bytes, stream) : cudaMalloc(ptr, bytes);
+        };
+        for (int b = 0; b < (p.qz() ? NUV : 1); ++b) {
+            CK(mal((void**)&U[b], blk));
+            CK(mal((void**)&V[b], blk));
+        }
+        CK(mal((void**)&Zr, rec));
+        CK(mal((void**)&Qr, rec));
+        CK(mal((void**)&Tr, tf));
+        CK(mal((void**)&prog, (size_t)(p.q + 1) * sizeof(int)));
+        if (k1p) {
+            CK(mal((void**)&k1prof, 12 * sizeof(long long)));
+            CK(cudaMemsetAsync(k1prof, 0, 12 * sizeof(long long), stream));
+        }
+        if (p.qz()) {
+            int lo = 0, hi = 0;
+            CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+            CK(cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, lo));  // lowest priority
+            for (int b = 0; b < NUV; ++b) {
+                CK(cudaEventCreateWithFlags(&ev_uv[b], cudaEventDisableTiming));
+                CK(cudaEventCreateWithFlags(&ev_qz[b], cudaEventDisableTiming));
+            }
+        }
+        return HT_OK;
+    }
+    int release(cudaStream_t stream, bool async_) {
+        if (k1prof) {
+            CK(cudaMemcpyAsync(k1prof_host, k1prof, sizeof(k1prof_host), cudaMemcpyDeviceToHost, stream));
+            CK(cudaStreamSynchronize(stream));
+        }
+        auto fr = [&](void* ptr) -> cudaError_t {
+            if (!ptr) return cudaSuccess;
+            return async_ ? cudaFreeAsync(ptr, stream) : cudaFree(ptr);
+        };
+        for (int b = 0; b < NUV; ++b) {
+            CK(fr(U[b]));
+            CK(fr(V[b]));
+        }
+        CK(fr(Zr));
+        CK(fr(Qr));
+        CK(fr(Tr));
+        CK(fr(prog));
+        CK(fr(k1prof));
+        for (int b = 0; b < NUV; ++b) {
+            if (ev_uv[b]) cudaEventDestroy(ev_uv[b]);
+            if (ev_qz[b]) cudaEventDestroy(ev_qz[b]);
+        }
+        if (side) cudaStreamDestroy(side);  // deferred until its work completes
+        return HT_OK;
+    }
+};
+
+void print_k1prof(const long long* h) {
+    const char* nm[12] = {"wait", "loads", "catchup", "QB+T", "larfgZ", "strip", "RQ", "larfgQ", "writes", "s9", "s10", "s11"};
+    double tot = 0;
+    for (int i = 0; i < 12; ++i) tot += (double)h[i];
+    fprintf(stderr, "K1 cycles (sum over CTAs):");
+    for (int i = 0; i < 12; ++i) fprintf(stderr, " %s=%.1f%%", nm[i], 100.0 * h[i] / (tot > 0 ? tot : 1));
+    fprintf(stderr, " total=%.3g\n", tot);
+}
+
+// Enqueue every group of the reduction: chase (K1) -> accumulate U/V (K2) -> H/T right and left
+// chains (K3/K4) on `stream`; Q/Z chains on the side stream.  With prof, per-class device
+// times are accumulated into g_last_ms (needs a host sync at the end).
+template <typename S>
+int enqueue_groups(const Plan<S>& p, Workspace<S>& ws, cudaStream_t stream, bool prof) {
+    const int n = p.n, r = p.r, q = p.q, WP = p.WP, LDB = p.LDB, TLD = q;
+    const bool qz = p.qz();
+    const int ngroups = (n - 2 + q - 1) / q;
+    static thread_local std::vector<cudaEvent_t> ev;  // grow-only pool (event creation is slow)
+    if (prof)
+        while (ev.size() < (size_t)5 * ngroups) {
+            cudaEvent_t e;
+            CK(cudaEventCreate(&e));
+            ev.push_back(e);
+        }
+    if (qz) {
+        CK(cudaEventRecord(ws.ev_qz[0], stream));  // workspace allocations visible to the side stream
+        CK(cudaStreamWaitEvent(ws.side, ws.ev_qz[0], 0));
+    }
+    int g = 0;
+    for (int j1 = 1; j1 <= n - 2; j1 += q, ++g) {
+        const int qp = std::min(q, n - 1 - j1);
+        const int K = 1 + (n - j1 - 2) / r;
+        const int bsel = qz ? (g % NUV) : 0;
+        if (prof) CK(cudaEventRecord(ev[5 * g + 0], stream));
+        CK(cudaMemsetAsync(ws.prog, 0, (size_t)(q + 1) * sizeof(int), stream));
+        CK(cudaMemsetAsync(ws.Qr, 0, (size_t)qp * K * (r + 1) * sizeof(S), stream));
+        CK(cudaMemsetAsync(ws.Zr, 0, (size_t)qp * K * (r + 1) * sizeof(S), stream));
+        ChaseArgs<S> ca{n, r, qp, j1, K, p.H, p.ldh, p.T, p.ldt, ws.Qr, ws.Zr, ws.Tr, TLD, ws.prog, p.strip_cap, ws.k1prof};
+        void* kargs[] = {&ca};
+        CK(cudaLaunchKernel(p.chase_fn, dim3(qp), dim3(CHASE_NT), kargs, p.chase_bytes, stream));
+        if (qz && g >= NUV) CK(cudaStreamWaitEvent(stream, ws.ev_qz[bsel], 0));  // Q/Z of g-NUV done with U/V[bsel]
+        AccumArgs<S> aa{n, r, qp, j1, K, WP, LDB, ws.Qr, ws.Zr, ws.U[bsel], ws.V[bsel]};
+        accum_kernel<S, ACC_NT><<<dim3(K, 2), ACC_NT, p.acc_bytes, stream>>>(aa);
+        CK(cudaGetLastError());
+        g_last_launches += 2;
+        if (qz) CK(cudaEventRecord(ws.ev_uv[bsel], stream));
+        if (prof) CK(cudaEventRecord(ev[5 * g + 1], stream));
+        // ---- apply phase: right updates of H, T (staircase + V_k), then left (U_k^*) ----
+        const int tiles = (n + CH_BM - 1) / CH_BM;
+        ChainParams<S> pr{n, r, qp, j1, K, {{p.H, p.ldh, ws.V[bsel], CM_AB_RIGHT, 0, tiles},
+                                            {p.T, p.ldt, ws.V[bsel], CM_AB_RIGHT, 0, tiles}}, 2, ws.Zr};
+        if (int rc = chain<S>(pr, WP, 2 * tiles, r, q, stream)) return rc;
+        ChainParams<S> pl{n, r, qp, j1, K, {{p.H, p.ldh, ws.U[bsel], CM_A_LEFT, 1, tiles},
+                                            {p.T, p.ldt, ws.U[bsel], CM_B_LEFT, 1, tiles}}, 2, ws.Zr};
+        if (int rc = chain<S>(pl, WP, 2 * tiles, r, q, stream)) return rc;
+        g_last_launches += 2;
+        if (prof) CK(cudaEventRecord(ev[5 * g + 2], stream));
+        // ---- Q <- Q U_k, Z <- Z V_k (row chains on the side stream; never read by the chase) ----
+        if (qz) {
+            CK(cudaStreamWaitEvent(ws.side, ws.ev_uv[bsel], 0));
+            if (prof) CK(cudaEventRecord(ev[5 * g + 3], ws.side));
+            ChainParams<S> pq{n, r, qp, j1, K, {{p.Q ? p.Q : p.Z, p.Q ? p.ldq : p.ldz, p.Q ? ws.U[bsel] : ws.V[bsel], CM_PLAIN, 0, tiles},
+                                                {p.Z, p.ldz, ws.V[bsel], CM_PLAIN, 0, tiles}},
+                              (p.Q && p.Z) ? 2 : 1, ws.Zr};
+            // persistent grid of ~half the SMs: the chase of the next group keeps whole SMs to start on
+            if (int rc = chain<S>(pq, WP, std::min(pq.njobs * tiles, p.qz_ctas), r, q, ws.side, 116 * 1024)) return rc;
+            if (prof) CK(cudaEventRecord(ev[5 * g + 4], ws.side));
+            CK(cudaEventRecord(ws.ev_qz[bsel], ws.side));
+            ++g_last_launches;
+        }
+    }
+    if (qz) {  // join the side stream back into the caller's stream
+        CK(cudaEventRecord(ws.ev_qz[0], ws.side));
+        CK(cudaStreamWaitEvent(stream, ws.ev_qz[0], 0));
+    }
+    if (prof) {
+        CK(cudaStreamSynchronize(stream));
+        double acc[3] = {0, 0, 0};
+        for (int i = 0; i < g; ++i)
+            for (int c = 0; c < 3; ++c) {
+                if (c == 2 && !qz) continue;
+                float x = 0;
+                const int e0 = c == 2 ? 3 : c;
+                CK(cudaEventElapsedTime(&x, ev[5 * i + e0], ev[5 * i + e0 + 1]));
+                acc[c] += x;
+            }
+        for (int c = 0; c < 3; ++c) g_last_ms[c] = acc[c];
+    }
+    return HT_OK;
+}
+
+// Cached CUDA graphs of the group loop, keyed by the full plan (sizes, q and buffer pointers);
+// each entry owns its workspace (plain cudaMalloc: graph nodes bake the pointers in).
+template <typename S>
+struct GraphEntry {
+    Plan<S> plan;
+    Workspace<S> ws;
+    cudaGraphExec_t exec = nullptr;
+    int64_t launches = 0;
+    int dev = -1;
+};
+
+template <typename S>
+int graph_for(const Plan<S>& p, cudaStream_t stream, GraphEntry<S>** out) {
+    static thread_local std::vector<GraphEntry<S>*> cache;
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    for (auto* e : cache)
+        if (e->dev == dev && e->plan.same(p)) {
+            *out = e;
+            return HT_OK;
+        }
+    if (cache.size() >= 4) {  // evict the oldest
+        GraphEntry<S>* old = cache.front();
+        cache.erase(cache.begin());
+        CK(cudaDeviceSynchronize());
+        cudaGraphExecDestroy(old->exec);
+        old->ws.release(stream, false);
+        delete old;
+    }
+    auto* e = new GraphEntry<S>();
+    e->plan = p;
+    e->dev = dev;
+    if (int rc = e->ws.alloc(p, stream, /*async=*/false, false)) {
+        delete e;
+        return rc;
+    }
+    cudaStream_t cap = nullptr;
+    CK(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+    const int64_t l0 = g_last_launches;
+    CK(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
+    int rc = enqueue_groups<S>(p, e->ws, cap, false);
+    cudaGraph_t graph = nullptr;
+    const cudaError_t ce = cudaStreamEndCapture(cap, &graph);
+    cudaStreamDestroy(cap);
+    e->launches = g_last_launches - l0;
+    g_last_launches = l0;
+    if (rc || ce != cudaSuccess) {
+        if (graph) cudaGraphDestroy(graph);
+        e->ws.release(stream, false);
+        delete e;
+        return rc ? rc : HT_ECUDA;
+    }
+    const cudaError_t ie = cudaGraphInstantiate(&e->exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (ie != cudaSuccess) {
+        e->ws.release(stream, false);
+        delete e;
+        return HT_ECUDA;
+    }
+    cache.push_back(e);
+    *out = e;
+    return HT_OK;
+}
 
 template <typename S>
 int run(int64_t n64, int64_t r64, S* H, int64_t ldh, S* T, int64_t ldt, S* Q, int64_t ldq, S* Z,
@@ -177,104 +442,32 @@ int run(int64_t n64, int64_t r64, S* H, int64_t ldh, S* T, int64_t ldt, S* Q, in
     CK(cudaFuncSetAttribute(chase_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)chase_bytes));
     CK(cudaFuncSetAttribute(accum_kernel<S, ACC_NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)acc_bytes));
 
-    // ---- workspace (stream-ordered) ----
-    S *U = nullptr, *V = nullptr, *Zr = nullptr, *Qr = nullptr, *Tr = nullptr;
-    int* prog = nullptr;
-    const size_t blk_elems = (size_t)Kmax * WP * LDB;
-    const size_t rec_elems = (size_t)q * Kmax * (r + 1);
-    const int TLD = q;
-    const size_t t_elems = (size_t)q * Kmax * TLD;
-    CK(cudaMallocAsync(&U, blk_elems * sizeof(S), stream));
-    CK(cudaMallocAsync(&V, blk_elems * sizeof(S), stream));
-    CK(cudaMallocAsync(&Zr, rec_elems * sizeof(S), stream));
-    CK(cudaMallocAsync(&Qr, rec_elems * sizeof(S), stream));
-    CK(cudaMallocAsync(&Tr, t_elems * sizeof(S), stream));
-    CK(cudaMallocAsync(&prog, (size_t)q * sizeof(int), stream));
-    long long* k1prof = nullptr;  // HT_K1PROF=1: chase phase cycle counts (stderr)
+    if (int rcp = chain_prepare<S>(WP)) return rcp;
+    Plan<S> pl{n, r, q, WP, LDB, Kmax, strip_cap, chase_bytes, acc_bytes, chase_fn, H, ldh, T, ldt, Q, ldq, Z, ldz,
+               std::max(8, nsm - q)};
     const bool k1p = getenv("HT_K1PROF") != nullptr;
-    if (k1p) {
-        CK(cudaMallocAsync(&k1prof, 12 * sizeof(long long), stream));
-        CK(cudaMemsetAsync(k1prof, 0, 12 * sizeof(long long), stream));
-    }
-
-    // kernel-class timing: 4 events per group from a pool, summed after one sync at the end
-    const int ngroups = (n - 2 + q - 1) / q;
-    std::vector<cudaEvent_t> ev;
-    if (prof) {
-        ev.resize((size_t)4 * ngroups);
-        for (auto& e : ev) CK(cudaEventCreate(&e));
-    }
-    int g = 0;
-
-    for (int j1 = 1; j1 <= n - 2; j1 += q) {
-        const int qp = std::min(q, n - 1 - j1);
-        const int K = 1 + (n - j1 - 2) / r;
-        if (prof) CK(cudaEventRecord(ev[4 * g + 0], stream));
-        CK(cudaMemsetAsync(prog, 0, (size_t)q * sizeof(int), stream));
-        CK(cudaMemsetAsync(Qr, 0, (size_t)qp * K * (r + 1) * sizeof(S), stream));
-        CK(cudaMemsetAsync(Zr, 0, (size_t)qp * K * (r + 1) * sizeof(S), stream));
-        ChaseArgs<S> ca{n, r, qp, j1, K, H, ldh, T, ldt, Qr, Zr, Tr, TLD, prog, strip_cap, k1prof};
-        void* kargs[] = {&ca};
-        CK(cudaLaunchCooperativeKernel(chase_fn, dim3(qp), dim3(CHASE_NT), kargs, chase_bytes, stream));
-        AccumArgs<S> aa{n, r, qp, j1, K, WP, LDB, Qr, Zr, U, V};
-        accum_kernel<S, ACC_NT><<<dim3(K, 2), ACC_NT, acc_bytes, stream>>>(aa);
-        g_last_launches += 2;
-        if (prof) CK(cudaEventRecord(ev[4 * g + 1], stream));
-        // ---- apply phase: right updates of H, T (staircase + V_k), then left (U_k^*) ----
-        const int tiles = (n + CH_BM - 1) / CH_BM;
-        ChainParams<S> pr{n, r, qp, j1, K, {{H, ldh, V, CM_AB_RIGHT, 0, tiles}, {T, ldt, V, CM_AB_RIGHT, 0, tiles}},
-                          2, Zr};
-        if (int rc = chain<S>(pr, WP, 2 * tiles, r, q, stream)) return rc;
-        ChainParams<S> pl{n, r, qp, j1, K, {{H, ldh, U, CM_A_LEFT, 1, tiles}, {T, ldt, U, CM_B_LEFT, 1, tiles}},
-                          2, Zr};
-        if (int rc = chain<S>(pl, WP, 2 * tiles, r, q, stream)) return rc;
-        g_last_launches += 2;
-        if (prof) CK(cudaEventRecord(ev[4 * g + 2], stream));
-        // ---- Q <- Q U_k, Z <- Z V_k (row chains; never read by the chase) ----
-        if (Q || Z) {
-            ChainParams<S> pq{n, r, qp, j1, K, {{Q ? Q : Z, Q ? ldq : ldz, Q ? U : V, CM_PLAIN, 0, tiles},
-                                                {Z, ldz, V, CM_PLAIN, 0, tiles}},
-                              (Q && Z) ? 2 : 1, Zr};
-            if (int rc = chain<S>(pq, WP, pq.njobs * tiles, r, q, stream)) return rc;
-            ++g_last_launches;
-        }
-        CK(cudaGetLastError());
-        if (prof) CK(cudaEventRecord(ev[4 * g + 3], stream));
-        ++g;
-    }
-    CK(cudaFreeAsync(U, stream));
-    CK(cudaFreeAsync(V, stream));
-    CK(cudaFreeAsync(Zr, stream));
-    CK(cudaFreeAsync(Qr, stream));
-    CK(cudaFreeAsync(Tr, stream));
-    CK(cudaFreeAsync(prog, stream));
-    if (k1p) {
-        long long h[12];
-        CK(cudaMemcpyAsync(h, k1prof, sizeof(h), cudaMemcpyDeviceToHost, stream));
-        CK(cudaStreamSynchronize(stream));
-        const char* nm[12] = {"wait", "loads", "catchup", "QB+T", "larfgZ", "strip", "RQ", "larfgQ", "writes", "s9", "s10", "s11"};
-        double tot = 0;
-        for (long long x : h) tot += (double)x;
-        fprintf(stderr, "K1 cycles (sum over CTAs):");
-        for (int i = 0; i < 12; ++i) fprintf(stderr, " %s=%.1f%%", nm[i], 100.0 * h[i] / tot);
-        fprintf(stderr, " total=%.3g\n", tot);
-        CK(cudaFreeAsync(k1prof, stream));
+    int rc = HT_OK;
+    if (prof || k1p || getenv("HT_NO_GRAPH")) {
+        // direct launches (per-kernel-class events / K1 phase counters need them)
+        Workspace<S> ws;
+        if ((rc = ws.alloc(pl, stream, /*async=*/true, k1p))) return rc;
+        rc = enqueue_groups<S>(pl, ws, stream, prof);
+        if (int rf = ws.release(stream, /*async=*/true)) rc = rc ? rc : rf;
+        if (rc) return rc;
+        if (k1p) print_k1prof(ws.k1prof_host);
+    } else {
+        // the whole group loop as one cached CUDA graph (one launch per call; no host stalls)
+        GraphEntry<S>* ge = nullptr;
+        if ((rc = graph_for<S>(pl, stream, &ge))) return rc;
+        CK(cudaGraphLaunch(ge->exec, stream));
+        g_last_launches += ge->launches;
     }
     CK(cudaEventRecord(e_end, stream));
     if (prof) {
         CK(cudaEventSynchronize(e_end));
         float tot = 0;
         CK(cudaEventElapsedTime(&tot, e_start, e_end));
-        double acc[3] = {0, 0, 0};
-        for (int i = 0; i < g; ++i)
-            for (int c = 0; c < 3; ++c) {
-                float x = 0;
-                CK(cudaEventElapsedTime(&x, ev[4 * i + c], ev[4 * i + c + 1]));
-                acc[c] += x;
-            }
-        for (int c = 0; c < 3; ++c) g_last_ms[c] = acc[c];
         g_last_ms[3] = tot;
-        for (auto& e : ev) cudaEventDestroy(e);
     }
     cudaEventDestroy(e_start);
     cudaEventDestroy(e_end);

@@ -80,3 +80,25 @@ __device__ __forceinline__ S warp_sum(S v) {
     for (int o = 16; o > 0; o >>= 1) v += shfl_xor(v, o);
     return v;
 }
+
+// Fast reciprocal / reciprocal square root for the chase's latency-bound scalar chains:
+// MUFU seed (rcp.approx / rsqrt.approx, ~2^-22 relative) + two Newton steps (full fp64 accuracy
+// to within a few ulp; not correctly rounded -- the oracle's sqrt/division differ in the last bits).
+__device__ __forceinline__ double fast_rcp(double x) {
+    double y;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    double e = fma(-x, y, 1.0);
+    y = fma(y, e, y);
+    e = fma(-x, y, 1.0);
+    return fma(y, e, y);
+}
+__device__ __forceinline__ double fast_rsqrt(double x) {
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    double h = x * y;
+    double e = fma(-h, y, 1.0);  // 1 - x y^2
+    y = fma(0.5 * e, y, y);
+    h = x * y;
+    e = fma(-h, y, 1.0);
+    return fma(0.5 * e, y, y);
+}

@@ -17,7 +17,7 @@ __global__ void bench(const double* C0, double* out, long long* cyc, int m, int 
     __syncthreads();
     long long t0 = clock64();
     for (int it = 0; it < reps; ++it) {
-        if (threadIdx.x < RQCfg<double, MAXM>::NTHR) rq_direction<double, MAXM>(m, Cb, m + 1, piv, &flag, uu);
+        if (threadIdx.x < rq_nthr<double, MAXM>()) rq_dir<double, MAXM>(m, Cb, m + 1, piv, &flag, uu);
         __syncthreads();
         if (threadIdx.x == 0) flag = 1 << 30;
         __syncthreads();
