@@ -6,8 +6,10 @@
 A step = one full ``ht_stage2`` call (all §8(a) rows: chase, accumulation, staircase,
 off-window and Q/Z updates) on the config's synthetic r-HT pencil, inputs restored from a
 pristine device copy inside the step (inputs 4 x n^2 x 8 B > 126 MB L2, so no L2 reuse across
-steps).  value = N x 10n^3 / t_step (the paper's standard count, PAPER.md:712) in GFLOP/s;
-N > 1 runs N independent replicas (weak scaling; sharding is a later §8(e) row).
+steps).  value = 10n^3 / t_step (the paper's standard count) in GFLOP/s.
+N > 1 (torchrun, one rank per GPU) solves ONE problem on N GPUs (strong scaling):
+the root chases and updates H, T; every rank updates its row slab of Q and Z from reflector
+records broadcast by NCCL per group; the slabs are gathered to the root inside the timed call.
 
 --impl reference times the CPU oracle (Alg. 2, plain C, all host cores) on a bounded sample of
 the same workload (the leading n_s x n_s sub-pencil of the config's pencil, same r and
@@ -130,7 +132,7 @@ def run_reference(args, rank):
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": v, "unit": "GFLOP/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.mean(times),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64" if not c["complex"] else "c128",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64" if not c["complex"] else "c128",
         "data": "synthetic", "config": _config_dict(args, c, q=None),
         "cpu_baseline": {"value": v, "unit": "GFLOP/s", "cores": cores, "kind": "oracle", "sample": sample},
         "e2e": {"value": v, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -142,7 +144,7 @@ def _config_dict(args, c, q):
                      f"T diag {'graded 10^U(-3,0)' if c['tdiag'] == 'graded' else '1+|N(0,1)|'}, Q,Z accumulated",
          "n": c["n"], "r": c["r"], "complex": c["complex"], "seed": c["seed"],
          "l2": "inputs (4 n^2 fp64) larger than the 126 MB L2; restored from a device copy each step",
-         "parallelism": f"replicas x{args.gpus}"}
+         "parallelism": (f"root chase + H/T, Q/Z row slabs x{args.gpus} (NCCL)" if args.gpus > 1 else "1 GPU")}
     if q is not None:
         d["q"] = q
     return d
@@ -162,6 +164,8 @@ def main():
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.gpus != world and args.impl == "ours":
+        print(f"warning: --gpus {args.gpus} but WORLD_SIZE={world}; using WORLD_SIZE", file=sys.stderr)
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
@@ -174,8 +178,10 @@ def main():
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    comm = None
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
+        comm = ht.comm_from_torch()
     c = CONFIGS[args.config]
     n, r, cplx = c["n"], c["r"], c["complex"]
     q = args.q or ht.default_q(n, r, cplx)
@@ -198,7 +204,7 @@ def main():
         T.copy_(T0)
         Qd.copy_(I0)
         Zd.copy_(I0)
-        ht.ht_stage2(H, T, r, Qd, Zd, stream=stream, q=q, profile=profile)
+        ht.ht_stage2(H, T, r, Qd, Zd, stream=stream, q=q, profile=profile, comm=comm)
 
     for _ in range(max(3, args.warmup)):
         step()
@@ -233,7 +239,7 @@ def main():
         ms_total = float(t.item())
     ms_step = ms_total / args.steps
     fstd = ht.flops_std(n, cplx)
-    value = world * fstd / (ms_step * 1e-3) / 1e9
+    value = fstd / (ms_step * 1e-3) / 1e9  # one problem on all ranks (strong scaling)
     brk = brk_ms
 
     # ---- roofline of the dominant kernel class (live CUDA-event durations) ----
@@ -261,12 +267,12 @@ def main():
 
     out = {
         "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
-        "warmup": max(3, args.warmup), "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "warmup": max(3, args.warmup), "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64" if not cplx else "c128", "data": "synthetic",
         "config": _config_dict(args, c, q),
         "roofline": roof,
         "fraction_fp64_roofline": value / (world * dmma * 1e3),
-        "gflops_counted": world * (fcnt_upd) / (ms_step * 1e-3) / 1e9,
+        "gflops_counted": fcnt_upd / (ms_step * 1e-3) / 1e9,
         "breakdown_ms": brk, "dmma_peak_tflops": dmma,
         "clocks": clk, "gpu_launches": launches,
         "measured_peaks": {k: peaks.get(k) for k in ("hbm_gbs", "bf16_tflops")},
@@ -286,7 +292,7 @@ def main():
             T.t().copy_(hp[1], non_blocking=True)
             Qd.t().copy_(ip, non_blocking=True)
             Zd.t().copy_(ip, non_blocking=True)
-            ht.ht_stage2(H, T, r, Qd, Zd, stream=stream, q=q)
+            ht.ht_stage2(H, T, r, Qd, Zd, stream=stream, q=q, comm=comm)
             for o, X in zip(outs, (H, T, Qd, Zd)):
                 o.copy_(X.t(), non_blocking=True)
         e1.record(stream)
@@ -297,7 +303,7 @@ def main():
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e_ms = float(t.item())
         esz = 16 if cplx else 8
-        out["e2e"] = {"value": world * fstd / (e_ms / args.steps * 1e-3) / 1e9, "unit": "GFLOP/s",
+        out["e2e"] = {"value": fstd / (e_ms / args.steps * 1e-3) / 1e9, "unit": "GFLOP/s",
                       "h2d_bytes_per_step": 4 * n * n * esz, "d2h_bytes_per_step": 4 * n * n * esz}
 
     if rank == 0 and not args.no_cpu:
@@ -310,6 +316,7 @@ def main():
     if rank == 0:
         print(json.dumps(out), flush=True)
     if world > 1:
+        ht.comm_destroy(comm)
         dist.destroy_process_group()
 
 

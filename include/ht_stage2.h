@@ -28,9 +28,13 @@
  * Q == NULL or Z == NULL skips that accumulation; H and T are then bitwise
  * identical to an accumulating run.
  *
- * Multi-GPU (comm != NULL): SPMD -- every rank calls the same function with
- * its own full-size buffers holding identical inputs; on return the result
- * is valid on opts->root (default 0); other ranks' Q/Z buffers are clobbered.
+ * Multi-GPU (comm != NULL): SPMD -- every rank calls the same function with its
+ * own full-size buffers holding identical inputs.  The root (opts->root, default 0) runs the
+ * chase and the H/T updates; per group of q sweeps it broadcasts the reflector records over
+ * NCCL, every rank forms the window blocks U_k, V_k and updates its row slab of Q and Z
+ * (ht_slab_range); at the end the slabs are gathered to the root.  On return H, T, Q, Z are
+ * valid on the root only; other ranks' buffers are clobbered.  Argument 13 (opts->root) out of
+ * range returns -13.
  *
  * Return codes (LAPACK INFO style):
  *    0  success
@@ -76,6 +80,8 @@ typedef struct ht_opts {
 
 #define HT_FLAG_NO_VALIDATE 1
 #define HT_FLAG_PROFILE 2 /* record per-kernel-class device times (ht_last_timing) */
+#define HT_FLAG_EMULATE_SLABS 4 /* comm == NULL: run the Q/Z updates as reserved[0] row slabs (testing the
+                                   multi-GPU decomposition on one GPU) */
 
 /* Real FP64 stage two.  Arguments 1..12 in order: n, r, H, ldh, T, ldt,
  * Q, ldq, Z, ldz, stream, comm. */
@@ -100,6 +106,10 @@ int ht_stage2_z_ex(int64_t n, int64_t r, cuDoubleComplex *H, int64_t ldh, cuDoub
 int ht_nccl_unique_id(void *id_out);
 int ht_comm_create(const void *id, int rank, int nranks, ncclComm_t *out);
 int ht_comm_destroy(ncclComm_t comm);
+
+/* Multi-GPU row slab: rows [*row0, *row0 + *nrows) (0-based) of Q and Z are updated
+ * by `rank` of `nranks` (whole 32-row tiles, balanced).  Host-only; returns 0 or -i. */
+int ht_slab_range(int64_t n, int nranks, int rank, int64_t *row0, int64_t *nrows);
 
 /* Human-readable text for a return code (static storage). */
 const char *ht_strerror(int code);

@@ -71,14 +71,58 @@ def _load():
     lib.ht_comm_create.restype = ctypes.c_int
     lib.ht_comm_destroy.argtypes = [p]
     lib.ht_comm_destroy.restype = ctypes.c_int
+    lib.ht_slab_range.argtypes = [i64, ctypes.c_int, ctypes.c_int, ctypes.POINTER(i64), ctypes.POINTER(i64)]
+    lib.ht_slab_range.restype = ctypes.c_int
     _lib = lib
     return lib
 
 
 EXPORTED_SYMBOLS = ("ht_stage2_d", "ht_stage2_z", "ht_stage2_d_ex", "ht_stage2_z_ex",
-                    "ht_nccl_unique_id", "ht_comm_create", "ht_comm_destroy", "ht_strerror",
+                    "ht_nccl_unique_id", "ht_comm_create", "ht_comm_destroy", "ht_slab_range", "ht_strerror",
                     "ht_flops_std", "ht_default_q", "ht_last_timing", "ht_probe_dmma_tflops",
                     "ht_probe_dfma_tflops")
+
+
+def slab_range(n: int, nranks: int, rank: int):
+    """(row0, nrows) of the Q/Z row slab rank `rank` of `nranks` updates (multi-GPU, C ABI)."""
+    a, b = ctypes.c_int64(), ctypes.c_int64()
+    rc = _load().ht_slab_range(int(n), int(nranks), int(rank), ctypes.byref(a), ctypes.byref(b))
+    if rc != 0:
+        raise HTError(rc)
+    return a.value, b.value
+
+
+def nccl_comm(rank: int, nranks: int, unique_id: bytes):
+    """Create an NCCL communicator (ht_comm_create) from a 128-byte unique id; returns an opaque int."""
+    out = ctypes.c_void_p()
+    buf = ctypes.create_string_buffer(bytes(unique_id), 128)
+    rc = _load().ht_comm_create(buf, int(rank), int(nranks), ctypes.byref(out))
+    if rc != 0:
+        raise HTError(rc)
+    return out.value
+
+
+def nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    rc = _load().ht_nccl_unique_id(buf)
+    if rc != 0:
+        raise HTError(rc)
+    return buf.raw
+
+
+def comm_from_torch(group=None):
+    """NCCL communicator over a torch.distributed process group (rank 0's unique id is broadcast
+    with broadcast_object_list: torch's own NCCL communicator is not exposed by a stable API)."""
+    import torch.distributed as dist
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    obj = [nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0, group=group)
+    return nccl_comm(rank, world, obj[0])
+
+
+def comm_destroy(comm) -> None:
+    if comm:
+        _load().ht_comm_destroy(ctypes.c_void_p(comm))
 
 
 def strerror(code: int) -> str:
@@ -124,7 +168,8 @@ def _check_mat(X, n, name, dtype):
 
 
 def ht_stage2(H, T, r: int, Q=None, Z=None, stream=None, q: int = 0, chase_ctas: int = 0,
-              validate: bool = True, profile: bool = False, comm=None):
+              validate: bool = True, profile: bool = False, comm=None, root: int = 0,
+              emulate_slabs: int = 0):
     """In-place stage two on device tensors (C ABI ``ht_stage2_{d,z}_ex``).
 
     H, T: n x n column-major CUDA tensors (float64 or complex128) holding an r-HT pencil.
@@ -142,8 +187,9 @@ def ht_stage2(H, T, r: int, Q=None, Z=None, stream=None, q: int = 0, chase_ctas:
     pq, ldq = _check_mat(Q, n, "Q", dt)
     pz, ldz = _check_mat(Z, n, "Z", dt)
     s = stream if stream is not None else torch.cuda.current_stream(H.device)
-    opts = Opts(q=int(q), chase_ctas=int(chase_ctas), root=0,
-                flags=(0 if validate else 1) | (2 if profile else 0))
+    opts = Opts(q=int(q), chase_ctas=int(chase_ctas), root=int(root),
+                flags=(0 if validate else 1) | (2 if profile else 0) | (4 if emulate_slabs > 1 else 0))
+    opts.reserved[0] = int(emulate_slabs)
     fn = lib.ht_stage2_z_ex if cplx else lib.ht_stage2_d_ex
     rc = fn(n, int(r), ph, ldh, pt, ldt, pq, ldq, pz, ldz, ctypes.c_void_p(s.cuda_stream),
             ctypes.c_void_p(comm) if comm else None, ctypes.byref(opts))

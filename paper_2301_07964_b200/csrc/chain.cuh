@@ -34,6 +34,7 @@ struct ChainJob {
     int mode;
     int trans;
     int ntiles;
+    int tile0;  // first tile of this job (row slab of a multi-GPU rank; 0 = whole matrix)
 };
 
 template <typename S>
@@ -166,7 +167,7 @@ __device__ __forceinline__ bool chain_tile(const ChainParams<S>& P, int bid, uns
     const ChainJob<S> J = P.job[jb_];
     const int mode = J.mode;
     const bool trans = J.trans != 0;
-    const int R0 = bid * CH_BM + 1;  // first tile row (1-based)
+    const int R0 = (J.tile0 + bid) * CH_BM + 1;  // first tile row (1-based)
     if (R0 > n) return false;
     const int nr = min(CH_BM, n - R0 + 1);
     const int R1 = R0 + nr - 1;

@@ -120,6 +120,29 @@ const void* chase_kernel_for(int r) {
 
 constexpr int ACC_NT = 256;
 
+// Row slab of rank i out of G for the Q/Z updates: whole chain tiles (CH_BM rows), balanced.
+inline void slab_tiles(int n, int G, int i, int* t0, int* nt) {
+    const int T = (n + CH_BM - 1) / CH_BM;
+    const int a = (int)((int64_t)T * i / G), b = (int)((int64_t)T * (i + 1) / G);
+    *t0 = a;
+    *nt = b - a;
+}
+
+template <typename S>
+ncclDataType_t nccl_type() { return ncclFloat64; }
+template <typename S>
+size_t nccl_count(size_t elems) { return elems * (sizeof(S) / sizeof(double)); }
+
+#define NK(x)                                                                     \
+    do {                                                                          \
+        ncclResult_t r_ = (x);                                                    \
+        if (r_ != ncclSuccess) {                                                  \
+            if (getenv("HT_DEBUG")) fprintf(stderr, "ht_stage2: NCCL %s at %s:%d\n", \
+                                            ncclGetErrorString(r_), __FILE__, __LINE__); \
+            return HT_ENCCL;                                                      \
+        }                                                                         \
+    } while (0)
+
 template <typename S>
 struct Plan {
     int n, r, q, WP, LDB, Kmax, strip_cap;
@@ -134,6 +157,11 @@ struct Plan {
     S* Z;
     int64_t ldz;
     int qz_ctas;
+    // multi-GPU: the root chases and updates H, T; every rank updates its row slab
+    // of Q and Z.  comm == nullptr: one GPU (emul > 1 splits the Q/Z chains into emulated slabs).
+    ncclComm_t comm = nullptr;
+    int rank = 0, nranks = 1, root = 0, emul = 1;
+    bool is_root() const { return comm == nullptr || rank == root; }
     bool qz() const { return Q || Z; }
     bool same(const Plan& o) const {
         return n == o.n && r == o.r && q == o.q && strip_cap == o.strip_cap && H == o.H && ldh == o.ldh &&
@@ -225,6 +253,54 @@ void print_k1prof(const long long* h) {
 // Enqueue every group of the reduction: chase (K1) -> accumulate U/V (K2) -> H/T right and left
 // chains (K3/K4) on `stream`; Q/Z chains on the side stream.  With prof, per-class device
 // times are accumulated into g_last_ms (needs a host sync at the end).
+// Final gather of the Q/Z row slabs to the root: each non-root rank packs its
+// rows of Q and Z into one contiguous buffer and sends it; the root unpacks rank by rank.
+template <typename S>
+int gather_slabs(const Plan<S>& p, cudaStream_t stream) {
+    const int n = p.n;
+    int maxnt = 0;
+    for (int i = 0; i < p.nranks; ++i) {
+        int t0, nt;
+        slab_tiles(n, p.nranks, i, &t0, &nt);
+        maxnt = std::max(maxnt, nt);
+    }
+    const size_t slab = (size_t)maxnt * CH_BM * n;
+    S* buf = nullptr;
+    CK(cudaMallocAsync(&buf, 2 * slab * sizeof(S), stream));
+    auto rows = [&](int i, int* a, int* len) {
+        int t0, nt;
+        slab_tiles(n, p.nranks, i, &t0, &nt);
+        *a = t0 * CH_BM;
+        *len = std::max(0, std::min(n, (t0 + nt) * CH_BM) - *a);
+    };
+    for (int i = 0; i < p.nranks; ++i) {
+        if (i == p.root) continue;
+        int a, len;
+        rows(i, &a, &len);
+        if (len == 0) continue;
+        const size_t cnt = nccl_count<S>((size_t)len * n);
+        if (p.rank == i) {
+            if (p.Q) pack_rows_kernel<S><<<4 * 148, 256, 0, stream>>>(p.Q, p.ldq, a, len, n, buf);
+            if (p.Z) pack_rows_kernel<S><<<4 * 148, 256, 0, stream>>>(p.Z, p.ldz, a, len, n, buf + slab);
+            CK(cudaGetLastError());
+            NK(ncclGroupStart());
+            if (p.Q) NK(ncclSend(buf, cnt, nccl_type<S>(), p.root, p.comm, stream));
+            if (p.Z) NK(ncclSend(buf + slab, cnt, nccl_type<S>(), p.root, p.comm, stream));
+            NK(ncclGroupEnd());
+        } else if (p.rank == p.root) {
+            NK(ncclGroupStart());
+            if (p.Q) NK(ncclRecv(buf, cnt, nccl_type<S>(), i, p.comm, stream));
+            if (p.Z) NK(ncclRecv(buf + slab, cnt, nccl_type<S>(), i, p.comm, stream));
+            NK(ncclGroupEnd());
+            if (p.Q) unpack_rows_kernel<S><<<4 * 148, 256, 0, stream>>>(p.Q, p.ldq, a, len, n, buf);
+            if (p.Z) unpack_rows_kernel<S><<<4 * 148, 256, 0, stream>>>(p.Z, p.ldz, a, len, n, buf + slab);
+            CK(cudaGetLastError());
+        }
+    }
+    CK(cudaFreeAsync(buf, stream));
+    return HT_OK;
+}
+
 template <typename S>
 int enqueue_groups(const Plan<S>& p, Workspace<S>& ws, cudaStream_t stream, bool prof) {
     const int n = p.n, r = p.r, q = p.q, WP = p.WP, LDB = p.LDB, TLD = q;
@@ -246,48 +322,71 @@ int enqueue_groups(const Plan<S>& p, Workspace<S>& ws, cudaStream_t stream, bool
         const int qp = std::min(q, n - 1 - j1);
         const int K = 1 + (n - j1 - 2) / r;
         const int bsel = qz ? (g % NUV) : 0;
+        const bool root = p.is_root();
         if (prof) CK(cudaEventRecord(ev[5 * g + 0], stream));
-        CK(cudaMemsetAsync(ws.prog, 0, (size_t)(q + 1) * sizeof(int), stream));
-        CK(cudaMemsetAsync(ws.Qr, 0, (size_t)qp * K * (r + 1) * sizeof(S), stream));
-        CK(cudaMemsetAsync(ws.Zr, 0, (size_t)qp * K * (r + 1) * sizeof(S), stream));
-        ChaseArgs<S> ca{n, r, qp, j1, K, p.H, p.ldh, p.T, p.ldt, ws.Qr, ws.Zr, ws.Tr, TLD, ws.prog, p.strip_cap, ws.k1prof};
-        void* kargs[] = {&ca};
-        CK(cudaLaunchKernel(p.chase_fn, dim3(qp), dim3(CHASE_NT), kargs, p.chase_bytes, stream));
+        if (root) {
+            CK(cudaMemsetAsync(ws.prog, 0, (size_t)(q + 1) * sizeof(int), stream));
+            CK(cudaMemsetAsync(ws.Qr, 0, (size_t)qp * K * (r + 1) * sizeof(S), stream));
+            CK(cudaMemsetAsync(ws.Zr, 0, (size_t)qp * K * (r + 1) * sizeof(S), stream));
+            ChaseArgs<S> ca{n, r, qp, j1, K, p.H, p.ldh, p.T, p.ldt, ws.Qr, ws.Zr, ws.Tr, TLD, ws.prog, p.strip_cap, ws.k1prof};
+            void* kargs[] = {&ca};
+            CK(cudaLaunchKernel(p.chase_fn, dim3(qp), dim3(CHASE_NT), kargs, p.chase_bytes, stream));
+        }
+        if (p.comm && qz) {  // the group's reflectors (2 qp K (r+1) scalars) from the root to every rank
+            const size_t cnt = nccl_count<S>((size_t)qp * K * (r + 1));
+            NK(ncclGroupStart());
+            NK(ncclBroadcast(ws.Qr, ws.Qr, cnt, nccl_type<S>(), p.root, p.comm, stream));
+            NK(ncclBroadcast(ws.Zr, ws.Zr, cnt, nccl_type<S>(), p.root, p.comm, stream));
+            NK(ncclGroupEnd());
+        }
         if (qz && g >= NUV) CK(cudaStreamWaitEvent(stream, ws.ev_qz[bsel], 0));  // Q/Z of g-NUV done with U/V[bsel]
         AccumArgs<S> aa{n, r, qp, j1, K, WP, LDB, ws.Qr, ws.Zr, ws.U[bsel], ws.V[bsel]};
-        accum_kernel<S, ACC_NT><<<dim3(K, 2), ACC_NT, p.acc_bytes, stream>>>(aa);
-        CK(cudaGetLastError());
-        g_last_launches += 2;
+        if (root || qz) {
+            accum_kernel<S, ACC_NT><<<dim3(K, 2), ACC_NT, p.acc_bytes, stream>>>(aa);
+            CK(cudaGetLastError());
+            g_last_launches += 2;
+        }
         if (qz) CK(cudaEventRecord(ws.ev_uv[bsel], stream));
         if (prof) CK(cudaEventRecord(ev[5 * g + 1], stream));
         // ---- apply phase: right updates of H, T (staircase + V_k), then left (U_k^*) ----
         const int tiles = (n + CH_BM - 1) / CH_BM;
-        ChainParams<S> pr{n, r, qp, j1, K, {{p.H, p.ldh, ws.V[bsel], CM_AB_RIGHT, 0, tiles},
-                                            {p.T, p.ldt, ws.V[bsel], CM_AB_RIGHT, 0, tiles}}, 2, ws.Zr};
-        if (int rc = chain<S>(pr, WP, 2 * tiles, r, q, stream)) return rc;
-        ChainParams<S> pl{n, r, qp, j1, K, {{p.H, p.ldh, ws.U[bsel], CM_A_LEFT, 1, tiles},
-                                            {p.T, p.ldt, ws.U[bsel], CM_B_LEFT, 1, tiles}}, 2, ws.Zr};
-        if (int rc = chain<S>(pl, WP, 2 * tiles, r, q, stream)) return rc;
-        g_last_launches += 2;
+        if (root) {
+            ChainParams<S> pr{n, r, qp, j1, K, {{p.H, p.ldh, ws.V[bsel], CM_AB_RIGHT, 0, tiles, 0},
+                                                {p.T, p.ldt, ws.V[bsel], CM_AB_RIGHT, 0, tiles, 0}}, 2, ws.Zr};
+            if (int rc = chain<S>(pr, WP, 2 * tiles, r, q, stream)) return rc;
+            ChainParams<S> pl{n, r, qp, j1, K, {{p.H, p.ldh, ws.U[bsel], CM_A_LEFT, 1, tiles, 0},
+                                                {p.T, p.ldt, ws.U[bsel], CM_B_LEFT, 1, tiles, 0}}, 2, ws.Zr};
+            if (int rc = chain<S>(pl, WP, 2 * tiles, r, q, stream)) return rc;
+            g_last_launches += 2;
+        }
         if (prof) CK(cudaEventRecord(ev[5 * g + 2], stream));
         // ---- Q <- Q U_k, Z <- Z V_k (row chains on the side stream; never read by the chase) ----
         if (qz) {
             CK(cudaStreamWaitEvent(ws.side, ws.ev_uv[bsel], 0));
             if (prof) CK(cudaEventRecord(ev[5 * g + 3], ws.side));
-            ChainParams<S> pq{n, r, qp, j1, K, {{p.Q ? p.Q : p.Z, p.Q ? p.ldq : p.ldz, p.Q ? ws.U[bsel] : ws.V[bsel], CM_PLAIN, 0, tiles},
-                                                {p.Z, p.ldz, ws.V[bsel], CM_PLAIN, 0, tiles}},
-                              (p.Q && p.Z) ? 2 : 1, ws.Zr};
-            // persistent grid of ~half the SMs: the chase of the next group keeps whole SMs to start on
-            if (int rc = chain<S>(pq, WP, std::min(pq.njobs * tiles, p.qz_ctas), r, q, ws.side, 116 * 1024)) return rc;
+            const int nslab = p.comm ? 1 : std::max(1, p.emul);
+            for (int sl = 0; sl < nslab; ++sl) {
+                int t0 = 0, nt = tiles;
+                if (p.comm) slab_tiles(n, p.nranks, p.rank, &t0, &nt);
+                else if (nslab > 1) slab_tiles(n, nslab, sl, &t0, &nt);
+                if (nt <= 0) continue;
+                ChainParams<S> pq{n, r, qp, j1, K, {{p.Q ? p.Q : p.Z, p.Q ? p.ldq : p.ldz, p.Q ? ws.U[bsel] : ws.V[bsel], CM_PLAIN, 0, nt, t0},
+                                                    {p.Z, p.ldz, ws.V[bsel], CM_PLAIN, 0, nt, t0}},
+                                  (p.Q && p.Z) ? 2 : 1, ws.Zr};
+                // persistent grid leaving q whole SMs: the chase of the next group starts at once
+                if (int rc = chain<S>(pq, WP, std::min(pq.njobs * nt, p.qz_ctas), r, q, ws.side, 116 * 1024)) return rc;
+                ++g_last_launches;
+            }
             if (prof) CK(cudaEventRecord(ev[5 * g + 4], ws.side));
             CK(cudaEventRecord(ws.ev_qz[bsel], ws.side));
-            ++g_last_launches;
         }
     }
     if (qz) {  // join the side stream back into the caller's stream
         CK(cudaEventRecord(ws.ev_qz[0], ws.side));
         CK(cudaStreamWaitEvent(stream, ws.ev_qz[0], 0));
     }
+    if (p.comm && qz && p.nranks > 1)
+        if (int rc = gather_slabs<S>(p, stream)) return rc;
     if (prof) {
         CK(cudaStreamSynchronize(stream));
         double acc[3] = {0, 0, 0};
@@ -383,7 +482,6 @@ int run(int64_t n64, int64_t r64, S* H, int64_t ldh, S* T, int64_t ldt, S* Q, in
     if (Q && ldq < std::max<int64_t>(1, n64)) return -8;
     if (Z && ldz < std::max<int64_t>(1, n64)) return -10;
     if (n64 > (1 << 30)) return -1;
-    if (comm != nullptr) return HT_EUNSUPPORTED;  // multi-GPU path: see DESIGN.md (next)
     if (n64 == 0) return HT_OK;
     for (void* p : {(void*)H, (void*)T, (void*)Q, (void*)Z}) {
         if (!p) continue;
@@ -445,9 +543,18 @@ int run(int64_t n64, int64_t r64, S* H, int64_t ldh, S* T, int64_t ldt, S* Q, in
     if (int rcp = chain_prepare<S>(WP)) return rcp;
     Plan<S> pl{n, r, q, WP, LDB, Kmax, strip_cap, chase_bytes, acc_bytes, chase_fn, H, ldh, T, ldt, Q, ldq, Z, ldz,
                std::max(8, nsm - q)};
+    if (comm) {
+        pl.comm = comm;
+        NK(ncclCommCount(comm, &pl.nranks));
+        NK(ncclCommUserRank(comm, &pl.rank));
+        pl.root = opts ? opts->root : 0;
+        if (pl.root < 0 || pl.root >= pl.nranks) return -13;
+    } else if (opts && (opts->flags & HT_FLAG_EMULATE_SLABS)) {
+        pl.emul = std::max(1, opts->reserved[0]);
+    }
     const bool k1p = getenv("HT_K1PROF") != nullptr;
     int rc = HT_OK;
-    if (prof || k1p || getenv("HT_NO_GRAPH")) {
+    if (prof || k1p || comm || getenv("HT_NO_GRAPH")) {
         // direct launches (per-kernel-class events / K1 phase counters need them)
         Workspace<S> ws;
         if ((rc = ws.alloc(pl, stream, /*async=*/true, k1p))) return rc;
@@ -521,6 +628,19 @@ int ht_comm_create(const void* id, int rank, int nranks, ncclComm_t* out) {
     ncclUniqueId uid;
     memcpy(&uid, id, sizeof(uid));
     return ncclCommInitRank(out, nranks, uid, rank) == ncclSuccess ? HT_OK : HT_ENCCL;
+}
+
+int ht_slab_range(int64_t n, int nranks, int rank, int64_t* row0, int64_t* nrows) {
+    if (n < 0) return -1;
+    if (nranks < 1) return -2;
+    if (rank < 0 || rank >= nranks) return -3;
+    if (!row0 || !nrows) return -4;
+    int t0 = 0, nt = 0;
+    slab_tiles((int)n, nranks, rank, &t0, &nt);
+    const int64_t a = (int64_t)t0 * CH_BM;
+    *row0 = std::min<int64_t>(a, n);
+    *nrows = std::max<int64_t>(0, std::min<int64_t>(n, (int64_t)(t0 + nt) * CH_BM) - *row0);
+    return HT_OK;
 }
 
 int ht_comm_destroy(ncclComm_t comm) {

@@ -79,3 +79,22 @@ __global__ void probe_dfma_kernel(int iters, double* out) {
     for (int i = 0; i < 8; ++i) s += acc[i];
     if (s == 12345.678) out[0] = s;
 }
+
+// Multi-GPU slab (un)packing: rows [a, a+len) of a column-major n-column matrix <-> a contiguous
+// buffer (column by column), for the final gather of the Q/Z row slabs to the root.
+template <typename S>
+__global__ void pack_rows_kernel(const S* M, int64_t ld, int a, int len, int ncols, S* buf) {
+    const int64_t total = (int64_t)len * ncols;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t c = e / len, i = e % len;
+        buf[e] = M[(a + i) + c * ld];
+    }
+}
+template <typename S>
+__global__ void unpack_rows_kernel(S* M, int64_t ld, int a, int len, int ncols, const S* buf) {
+    const int64_t total = (int64_t)len * ncols;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t c = e / len, i = e % len;
+        M[(a + i) + c * ld] = buf[e];
+    }
+}

@@ -175,3 +175,41 @@ def test_error_codes():
     with pytest.raises(ht.HTError) as e:
         ht.ht_stage2(Hd, _dev(T), -1)
     assert e.value.code == -2
+
+
+# ---------------------------------------------------------------------------- multi-GPU decomposition
+# (SURVEY §8(e)).  gpurun and the driver give one GPU, and ranks that wait on one another must not
+# share a GPU, so the N>1 path is checked by (a) the same Q/Z row-slab decomposition run as
+# emulated slabs on one GPU, and (b) the NCCL path itself with a single-rank communicator.
+
+@pytest.mark.parametrize("slabs", [2, 3, 8])
+def test_emulated_row_slabs_bitwise_equal(slabs):
+    ht = _ht()
+    H, T = make_pencil(300, 10, seed=31)
+    outs = []
+    for emu in (0, slabs):
+        Hd, Td = _dev(H), _dev(T)
+        Qd, Zd = _dev(np.eye(300)), _dev(np.eye(300))
+        ht.ht_stage2(Hd, Td, 10, Qd, Zd, q=12, emulate_slabs=emu)
+        torch.cuda.synchronize()
+        outs.append([_host(X) for X in (Hd, Td, Qd, Zd)])
+    for a, b in zip(*outs):
+        assert np.array_equal(a, b)
+
+
+def test_single_rank_nccl_comm_bitwise_equal():
+    ht = _ht()
+    comm = ht.nccl_comm(0, 1, ht.nccl_unique_id())
+    try:
+        H, T = make_pencil(257, 9, seed=32)
+        outs = []
+        for c in (None, comm):
+            Hd, Td = _dev(H), _dev(T)
+            Qd, Zd = _dev(np.eye(257)), _dev(np.eye(257))
+            ht.ht_stage2(Hd, Td, 9, Qd, Zd, q=13, comm=c)
+            torch.cuda.synchronize()
+            outs.append([_host(X) for X in (Hd, Td, Qd, Zd)])
+        for a, b in zip(*outs):
+            assert np.array_equal(a, b)
+    finally:
+        ht.comm_destroy(comm)
