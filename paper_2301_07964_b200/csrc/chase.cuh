@@ -110,6 +110,8 @@ __device__ __forceinline__ void warp_larfg(int m, const S* x, S* vout, S& tau, d
 // a stage does not touch (H_i acts on columns 0..i) is warp-uniform, in sub-blocks of SB.
 // Group A carries the sequential chain (pivot rows, scalars); group B only consumes each stage's
 // pivot row and scalars from a shared-memory ring and trails it (never blocks group A).
+// For MAXM > 64 the [C; P] rows do not fit the register file: group B is dropped (NOB) and
+// Q~^* e1 = H_{m-1}...H_0 e1 is formed afterwards by one warp from the stored reflectors.
 template <typename S, int MAXM>
 struct RQCfg {
     static constexpr int LPR = (MAXM >= 16) ? 2 : 1;
@@ -118,7 +120,8 @@ struct RQCfg {
     static constexpr int NSB = (E + SB - 1) / SB;
     static constexpr int ROWT = MAXM * LPR;
     static constexpr int NA = (ROWT < 32) ? 32 : ROWT;
-    static constexpr int NTHR = 2 * NA;
+    static constexpr bool NOB = MAXM > 64;
+    static constexpr int NTHR = NOB ? NA : 2 * NA;
     static constexpr int PLD = LPR * NSB * SB + 4;  // ring slot: pivot row (de-interleaved) + K1, K2
 };
 
@@ -169,7 +172,8 @@ __device__ __forceinline__ void rq_direction(int m, const S* Cb, int LDC, S* rin
                 for (int e = 0; e < SB; ++e) dst[sb * SB + e] = row[sb * SB + e];
     };
     // per-stage local work: g, nx (partial over my columns < i), ri
-    S bk[EP];
+    constexpr bool NOB = CF::NOB;
+    S bk[NOB ? 1 : EP];
     auto dots = [&](const S* pv, int i, S& g, double& nx, S& ri) {
         const int eth = (i - part + LPR - 1) / LPR;  // my elements e < eth have column < i
         const int sbi = eth / SB;
@@ -184,7 +188,7 @@ __device__ __forceinline__ void rq_direction(int m, const S* Cb, int LDC, S* rin
                 for (int e = 0; e < SB; ++e) {
                     const int ee = sb * SB + e;
                     const S b = (ee < eth) ? pv[part * EP + ee] : S(0.0);
-                    bk[ee] = b;
+                    if constexpr (!NOB) bk[ee] = b;
                     if (e & 1) {
                         n1 += abs2(b);
                         g1 = fma_s(row[ee], conjv(b), g1);
@@ -200,18 +204,27 @@ __device__ __forceinline__ void rq_direction(int m, const S* Cb, int LDC, S* rin
         g = g0 + g1;
         nx = n0 + n1;
     };
-    auto update = [&](int i, S f) {  // bk (zero for columns >= i) from dots()
+    auto update = [&](const S* pv, int i, S f) {  // bk (zero for columns >= i) from dots()
+        const int eth = (i - part + LPR - 1) / LPR;
 #pragma unroll
         for (int sb = 0; sb < NSB; ++sb) {
             if (sb * SB * LPR <= i) {
 #pragma unroll
-                for (int e = 0; e < SB; ++e) row[sb * SB + e] -= f * bk[sb * SB + e];
+                for (int e = 0; e < SB; ++e) {
+                    const int ee = sb * SB + e;
+                    if constexpr (NOB) {
+                        if (ee < eth) row[ee] -= f * pv[part * EP + ee];
+                    } else {
+                        row[ee] -= f * bk[ee];
+                    }
+                }
             }
         }
     };
     const int ilast = (sizeof(S) == 8) ? 1 : 0;
     if (!grpB) {
         // ---------------- group A: C rows, the sequential chain ----------------
+        syncA();  // every row is in registers before the ring (which may overlay Cb) is written
         if (live && l == m - 1) write_pivot(m - 1, m);
         syncA();
         for (int i = m - 1; i >= 1; --i) {
@@ -238,14 +251,14 @@ __device__ __forceinline__ void rq_direction(int m, const S* Cb, int LDC, S* rin
             }
             S f = K1 * (g + K2 * ri);
             if (!(live && l < i)) f = S(0.0);
-            update(i, f);
+            update(pv, i, f);
             if (gt == 0) {
                 ring[(size_t)i * PLD + LPR * EP] = K1;
                 ring[(size_t)i * PLD + LPR * EP + 1] = K2;
             }
             if (live && l == i - 1) write_pivot(i - 1, i);
             syncA();
-            if (gt == 0) st_release_cta(flag, i);  // stage i (pivot, K1, K2) complete
+            if (!NOB && gt == 0) st_release_cta(flag, i);  // stage i (pivot, K1, K2) complete
         }
         if constexpr (sizeof(S) != 8) {
             // stage 0: H_0 = I - tau e1 e1^* makes R~(0,0) real; P rows get row[0] *= (1 - tau)
@@ -258,7 +271,51 @@ __device__ __forceinline__ void rq_direction(int m, const S* Cb, int LDC, S* rin
             }
             if (gt == 0) {
                 ring[LPR * EP] = tau;
-                st_release_cta(flag, 0);
+                if (!NOB) st_release_cta(flag, 0);
+            }
+        }
+        if constexpr (NOB) {
+            // uu = H_{m-1} ... H_1 H_0 e1 from the stored reflectors (one warp; H_0 first).
+            // H_i = I - tau h h^*, h_c = conj(C[i][c]) / K2 (c < i), h_i = 1, tau = K1 |K2|^2.
+            syncA();
+            if (gt < 32) {
+                const int lane = gt;
+                constexpr int YL = (MAXM + 31) / 32;
+                S y[YL];
+#pragma unroll
+                for (int s2 = 0; s2 < YL; ++s2) y[s2] = S((lane + 32 * s2) == 0 ? 1.0 : 0.0);
+                if constexpr (sizeof(S) != 8) {
+                    const S tau0 = ring[LPR * EP];
+                    if (lane == 0) y[0] -= tau0 * y[0];
+                }
+                for (int i = 1; i <= m - 1; ++i) {
+                    const S* pv = ring + (size_t)i * PLD;
+                    const S K1 = pv[LPR * EP], K2 = pv[LPR * EP + 1];
+                    if (is_zero(K1)) continue;  // uniform
+                    S sacc = S(0.0);
+                    S yi = S(0.0);
+#pragma unroll
+                    for (int s2 = 0; s2 < YL; ++s2) {
+                        const int c = lane + 32 * s2;
+                        if (c < i) sacc = fma_s(pv[(c % LPR) * EP + c / LPR], y[s2], sacc);
+                        if (c == i) yi = y[s2];
+                    }
+                    sacc = warp_sum(sacc);
+                    yi = warp_sum(yi);
+                    const S inv = recip(K2);
+                    const S d = sacc * conjv(inv) + yi;
+                    const S tau = K1 * abs2(K2);
+                    const S td = tau * d;
+#pragma unroll
+                    for (int s2 = 0; s2 < YL; ++s2) {
+                        const int c = lane + 32 * s2;
+                        if (c < i) y[s2] -= td * inv * conjv(pv[(c % LPR) * EP + c / LPR]);
+                        else if (c == i) y[s2] -= td;
+                    }
+                }
+#pragma unroll
+                for (int s2 = 0; s2 < YL; ++s2)
+                    if (lane + 32 * s2 < m) uu[lane + 32 * s2] = y[s2];
             }
         }
     } else {
@@ -279,7 +336,7 @@ __device__ __forceinline__ void rq_direction(int m, const S* Cb, int LDC, S* rin
             ri = lpr_sum<S, LPR>(ri);
             S f = K1 * (g + K2 * ri);
             if (!live) f = S(0.0);
-            update(i, f);
+            update(pv, i, f);
         }
         if (live && part == 0) uu[l] = row[0];
     }
@@ -410,10 +467,11 @@ template <typename S>
 __host__ __device__ inline size_t chase_smem_elems(int r, int qp, int strip_cap) {
     const int w = qp + r - 1;
     const size_t XL = (size_t)(w + r + 8);
+    const bool overlay = r > 64;         // the RQ ring (r slots of 132 for MAXM = 128) overlays the B block
     return 3 * XL +                      // x (2 buffers), y
-           (size_t)r * (r + 1) +         // B block
+           (overlay ? (size_t)r * 132 : (size_t)r * (r + 1)) +  // B block (| RQ ring)
            3 * (size_t)(r + 8) +         // vq, vz, uu
-           (size_t)r * (r + 20) +        // RQ ring (pivot rows + scalars per stage)
+           (overlay ? 0 : (size_t)r * (r + 20)) +  // RQ ring (pivot rows + scalars per stage)
            16 +                          // scalars
            (size_t)qp * (r + 1) +        // catch-up records (Y)
            (size_t)qp * (qp + 1) +       // T factor of window k
@@ -434,12 +492,14 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
     const int TL = qp + 1;
     S* xc[2] = {sm, sm + XL};  // column jb of this step / of the next step
     S* ys = sm + 2 * XL;
+    constexpr bool OVERLAY = MAXM > 64;  // RQ ring overlays Cb (the block goes to HBM after Q^*)
     S* Cb = ys + XL;           // r x (r+1) col-major
-    S* vq = Cb + (size_t)r * (r + 1);
+    static_assert(!OVERLAY || RQCfg<S, MAXM>::PLD <= 132, "ring slot of the overlay");
+    S* vq = Cb + (OVERLAY ? (size_t)r * 132 : (size_t)r * (r + 1));
     S* vz = vq + (r + 8);
     S* uu = vz + (r + 8);
-    S* ring = uu + (r + 8);    // RQ ring: r x (r+20)
-    S* scal = ring + (size_t)r * (r + 20);
+    S* ring = OVERLAY ? Cb : uu + (r + 8);  // RQ ring: r x (r+20) (overlay: r x 132)
+    S* scal = uu + (r + 8) + (OVERLAY ? 0 : (size_t)r * (r + 20));
     __shared__ int rq_flag;
     if (threadIdx.x == 0) rq_flag = 1 << 30;
     S* rec = scal + 16;        // qp x (r+1): v of Q_k^{j1+s}, tau at [r]
@@ -657,6 +717,11 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
                     }
                 }
                 __syncthreads();
+                if constexpr (OVERLAY) {  // the block goes to HBM: the RQ ring reuses its smem
+                    for (int cc = warp; cc < m; cc += NW)
+                        for (int ii = lane; ii < m; ii += 32) IDX(a.B, a.ldb, i1 + ii, i1 + cc) = Cb[ii + cc * LDC];
+                    __syncthreads();
+                }
                 K1_TICK(3);
                 // ---- (S5) RQ of the block -> Z_k^j ---------------------------------------------
                 if (tid < rq_nthr<S, MAXM>()) rq_dir<S, MAXM>(m, Cb, LDC, ring, &rq_flag, uu);
@@ -675,47 +740,65 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
                 // ---- (S6) right reflector Z_k^j on the band, next column ----------------------
                 const int nBb = max(0, i2 - i4 + 1);  // B rows i4..i2 (block rows i1..i2 from Cb)
                 const int bn = b0 + r;                 // first row of the next step's column
-                for (int e = tid; e < nA + nBb; e += NT) {
+                // SPR threads per row (adjacent lanes), CPR columns each, dot by shuffle-xor
+                constexpr int SPR = (MAXM * (int)sizeof(S) > 256) ? MAXM * (int)sizeof(S) / 256 : 1;
+                constexpr int CPR = MAXM / SPR;
+                const int part = tid % SPR, c0 = part * CPR;
+                const int nrows = nA + nBb;
+                for (int eb = tid / SPR; eb - tid / SPR < nrows; eb += NT / SPR) {  // uniform trip count per warp
+                    const int e = eb;
+                    const bool act = e < nrows;
                     const bool isA = e < nA;
                     const int row = isA ? i4 + e : i4 + (e - nA);
-                    S v[MAXM];
+                    S v[CPR];
                     S* gp = isA ? &IDX(a.A, a.lda, row, i1) : &IDX(a.B, a.ldb, row, i1);
                     const int64_t ld = isA ? a.lda : a.ldb;
-                    if (isA && e < stA) {
+                    if (act) {
+                        if (isA && e < stA) {
 #pragma unroll
-                        for (int c = 0; c < MAXM; ++c)
-                            if (c < m) v[c] = strip[e * SLD + c];
-                    } else if (!isA && row >= i1) {
+                            for (int c = 0; c < CPR; ++c)
+                                if (c0 + c < m) v[c] = strip[e * SLD + c0 + c];
+                        } else if (!OVERLAY && !isA && row >= i1) {
 #pragma unroll
-                        for (int c = 0; c < MAXM; ++c)
-                            if (c < m) v[c] = Cb[(row - i1) + c * LDC];
-                    } else if (!isA && (e - nA) < stB) {
+                            for (int c = 0; c < CPR; ++c)
+                                if (c0 + c < m) v[c] = Cb[(row - i1) + (c0 + c) * LDC];
+                        } else if (!isA && row < i1 && (e - nA) < stB) {
 #pragma unroll
-                        for (int c = 0; c < MAXM; ++c)
-                            if (c < m) v[c] = strip[(stA + e - nA) * SLD + c];
-                    } else {
+                            for (int c = 0; c < CPR; ++c)
+                                if (c0 + c < m) v[c] = strip[(stA + e - nA) * SLD + c0 + c];
+                        } else {
 #pragma unroll
-                        for (int c = 0; c < MAXM; ++c)
-                            if (c < m) v[c] = ldcg(gp + c * ld);
+                            for (int c = 0; c < CPR; ++c)
+                                if (c0 + c < m) v[c] = ldcg(gp + (c0 + c) * ld);
+                        }
                     }
-                    if (!is_zero(sig)) {
-                        S s0 = S(0.0), s1 = S(0.0);
+                    S s0 = S(0.0), s1 = S(0.0);
+                    if (act && !is_zero(sig)) {
 #pragma unroll
-                        for (int c = 0; c < MAXM; ++c)
-                            if (c < m) {
-                                if (c & 1) s1 = fma_s(v[c], vz[c], s1);
-                                else s0 = fma_s(v[c], vz[c], s0);
+                        for (int c = 0; c < CPR; ++c)
+                            if (c0 + c < m) {
+                                if (c & 1) s1 = fma_s(v[c], vz[c0 + c], s1);
+                                else s0 = fma_s(v[c], vz[c0 + c], s0);
                             }
-                        const S s = (s0 + s1) * sig;
-#pragma unroll
-                        for (int c = 0; c < MAXM; ++c)
-                            if (c < m) v[c] -= s * conjv(vz[c]);
                     }
-                    if (!isA && row > i1) v[0] = S(0.0);  // B(i1+1:i2,i1) = 0 (reading c5)
+                    S sdot = s0 + s1;
+                    if constexpr (SPR > 1) {
 #pragma unroll
-                    for (int c = 0; c < MAXM; ++c)
-                        if (c < m) gp[c * ld] = v[c];
-                    if (isA && row >= bn) xnext[row - bn] = v[0];  // column jb of step k+1
+                        for (int o = 1; o < SPR; o <<= 1) sdot += shfl_xor(sdot, o);
+                    }
+                    if (act) {
+                        if (!is_zero(sig)) {
+                            const S sv = sdot * sig;
+#pragma unroll
+                            for (int c = 0; c < CPR; ++c)
+                                if (c0 + c < m) v[c] -= sv * conjv(vz[c0 + c]);
+                        }
+                        if (!isA && row > i1 && part == 0) v[0] = S(0.0);  // B(i1+1:i2,i1) = 0 (reading c5)
+#pragma unroll
+                        for (int c = 0; c < CPR; ++c)
+                            if (c0 + c < m) gp[(c0 + c) * ld] = v[c];
+                        if (isA && row >= bn && part == 0) xnext[row - bn] = v[0];  // column jb of step k+1
+                    }
                 }
                 S* zr = a.Zr + ((int64_t)t * K + k) * (r + 1);
                 for (int c = tid; c < m; c += NT) zr[c] = vz[c];

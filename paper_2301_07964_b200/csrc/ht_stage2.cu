@@ -43,9 +43,12 @@ int64_t default_q(int64_t n, int64_t r, int is_complex) {
     (void)is_complex;
     const char* env = getenv("HT_Q");
     if (env && atoll(env) > 0) return atoll(env);
-    int64_t q = r;  // executed/useful flops of dense U/V ~ (q+r-1)^2/(2qr), minimal at q ~ r
-    if (q < 8) q = 8;
-    if (q > 64) q = 64;
+    // q = 2r up to 32: dense U/V execute (q+r-1)^2/(2qr) x the useful flops (minimal at q ~ r),
+    // while the group-serial chase's critical path n^2/(2rq) + 3n favours larger q (measured at
+    // config 2: q = 32 beats q = 16 by 1.4x); the window order w = q+r-1 must stay <= 160 (K2
+    // holds a w x w block in shared memory)
+    int64_t q = std::min<int64_t>(std::max<int64_t>(2 * r, 8), 32);
+    q = std::min<int64_t>(q, std::max<int64_t>(1, 161 - r));
     return std::max<int64_t>(1, std::min<int64_t>(q, std::max<int64_t>(1, n - 2)));
 }
 
@@ -112,8 +115,9 @@ const void* chase_kernel_for(int r) {
     if (r <= 8) return (const void*)chase_kernel<S, CHASE_NT, 8>;
     if (r <= 16) return (const void*)chase_kernel<S, CHASE_NT, 16>;
     if (r <= 32) return (const void*)chase_kernel<S, CHASE_NT, 32>;
-    if constexpr (sizeof(S) == 8) {
+    if constexpr (sizeof(S) == 8) {  // complex: r <= 32 (registers of the complex RQ)
         if (r <= 64) return (const void*)chase_kernel<S, CHASE_NT, 64>;
+        if (r <= 128) return (const void*)chase_kernel<S, CHASE_NT, 128>;
     }
     return nullptr;
 }

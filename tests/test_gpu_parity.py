@@ -65,6 +65,8 @@ CASES = [
     # (n, r, q): several windows and groups, ragged tails, q < r, q = r, q > r, q = 1
     (40, 3, 4), (64, 4, 4), (97, 6, 5), (100, 8, 17), (128, 16, 16), (131, 5, 1),
     (150, 7, 9), (77, 3, 12), (200, 16, 8), (257, 9, 13), (96, 2, 3), (60, 20, 7),
+    # r in (32, 64] and (64, 128]: split-row strips, RQ without the P group (r > 64)
+    (300, 40, 9), (330, 64, 32), (420, 128, 16), (260, 100, 33), (200, 77, 1),
 ]
 
 
@@ -111,10 +113,21 @@ def test_dense_H_r_ge_n_minus_1(n, r):
     check_parity(H, T, r)
 
 
-def test_graded_T_invariants_only():
-    # config-5 generator shape (graded T diagonal 10^U(-3,0)): forward parity unpinnable [V3]
-    H, T = make_pencil(512, 32, tdiag="graded", seed=1005)
-    check_parity(H, T, 32, fwd=False)
+@pytest.mark.parametrize("n,r,q", [(512, 32, 0), (640, 128, 32)])
+def test_graded_T_invariants_only(n, r, q):
+    # config-5 generator shape (graded T diagonal 10^U(-3,0), r up to 128): forward parity is
+    # unpinnable there [V3], so invariants only
+    H, T = make_pencil(n, r, tdiag="graded", seed=1005)
+    check_parity(H, T, r, q=q, fwd=False)
+
+
+@pytest.mark.parametrize("cfg,n", [(2, 1024), (3, 384), (4, 768), (5, 640)])
+def test_baseline_config_shapes_reduced_n(cfg, n):
+    # every BASELINE config's generator, r and field at a size the oracle finishes in seconds
+    from synth.pencil import CONFIGS
+    c = CONFIGS[cfg]
+    H, T = config_pencil(cfg, n)
+    check_parity(H, T, c["r"], fwd=(c["tdiag"] != "graded"))
 
 
 def test_singular_T():
