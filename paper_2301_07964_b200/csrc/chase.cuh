@@ -34,8 +34,10 @@ struct ChaseArgs {
     S* Zr;      // (qp*K) records of (r+1): v of Z_k^j, sigma at [r]
     S* Tr;      // (qp*K) records of TLD: column t of window k's WY factor T (rows 0..t)
     int TLD;
-    int* prog;  // qp counters: steps completed by each sweep of the group; prog[qp] = sweep ticket
+    int* prog;  // prog[0..qp): steps completed by each sweep; prog[qp]: ticket;
+                // prog[qp+1 .. 2qp+1): far-strip items completed by each helper
     int strip_cap;  // strip rows (A then B) staged in shared memory per step
+    int helpers;    // 1: far strips (rows above b0(k-1)) go to one helper CTA per sweep
     long long* prof;  // optional: per-CTA cycle counts of the step phases (8 slots)
 };
 
@@ -239,14 +241,15 @@ __device__ __forceinline__ void rq_direction(int m, const S* Cb, int LDC, S* rin
             S K1 = S(0.0), K2 = S(0.0);
             if (!(nx == 0.0 && im(alpha) == 0.0)) {  // uniform
                 const double s2 = abs2(alpha) + nx;
-                const double nrm = sqrt(s2);
+                const double y = fast_rsqrt(s2);
+                const double nrm = s2 * y;
                 const double beta = (re(alpha) >= 0.0) ? -nrm : nrm;
                 K2 = alpha - S(beta);
                 if constexpr (sizeof(S) == 8) {
-                    K1 = S(1.0 / (s2 + fabs(re(alpha)) * nrm));
+                    K1 = S(fast_rcp(s2 + fabs(re(alpha)) * nrm));
                 } else {
-                    const S tau = (S(beta) - alpha) * (1.0 / beta);
-                    K1 = tau * (1.0 / abs2(K2));
+                    const S tau = (S(beta) - alpha) * ((re(alpha) >= 0.0) ? -y : y);  // 1/beta
+                    K1 = tau * fast_rcp(abs2(K2));
                 }
             }
             S f = K1 * (g + K2 * ri);
@@ -479,6 +482,92 @@ __host__ __device__ inline size_t chase_smem_elems(int r, int qp, int strip_cap)
            (size_t)strip_cap * (r + 1);  // staged strip rows
 }
 
+// Far-strip helper of sweep t (one CTA per sweep): applies Z_k^j to the generate band's rows
+// above b0(k-1) = j1+(k-1)r+1 -- A rows [i4, b0(k-1)) and B rows [i4, b0(k-1)) of columns
+// i1..i2 -- which no step of the group reads before sweep j+1 reaches window k-1.  Order
+// (the same per-row reflector order as Alg. 3): item (t,k) after sweep t's step k (its Z record)
+// and after helper t-1's item k+1 (lag as the sweeps).  Sweep t+1 waits for helper t before its
+// step k-1 (see chase_kernel).
+template <typename S, int NT, int MAXM>
+__device__ __forceinline__ void far_strip_helper(const ChaseArgs<S>& a, int t, S* sm) {
+    const int n = a.n, r = a.r, qp = a.qp, j1 = a.j1, K = a.K;
+    const int j = j1 + t;
+    const int kcount = min(K, 2 + (n - j - 1) / r);
+    const int kprev = (t > 0) ? min(K, 2 + (n - j) / r) : 0;
+    int* hprog = a.prog + qp + 1;
+    const int tid = threadIdx.x;
+    S* zv = sm;
+    constexpr int SPR = (MAXM * (int)sizeof(S) > 256) ? MAXM * (int)sizeof(S) / 256 : 1;
+    constexpr int CPR = MAXM / SPR;
+    const int part = tid % SPR, c0 = part * CPR;
+    for (int k = 0; k < kcount; ++k) {
+        if (tid == 0) {
+            if (ld_acquire(&a.prog[t]) < k + 1)
+                while (ld_relaxed(&a.prog[t]) < k + 1) {
+                }
+            if (t > 0) {
+                const int need = min(k + 2, kprev);
+                while (ld_relaxed(&hprog[t - 1]) < need) {
+                }
+            }
+            (void)ld_acquire(&a.prog[t]);
+            if (t > 0) (void)ld_acquire(&hprog[t - 1]);
+        }
+        __syncthreads();
+        const int i1 = j + k * r + 1;
+        const int i2 = min(j + (k + 1) * r, n);
+        const int i3 = min(j + (k + 2) * r, n);
+        const int i4 = j1 + 1 + max(0, (k + t - qp + 1) * r);
+        const int m = i2 - i1 + 1;
+        const int cF = j1 + (k - 1) * r + 1;
+        const int nAf = max(0, min(cF, i3 + 1) - i4), nBf = max(0, min(cF, i2 + 1) - i4);
+        if (m >= 2 && nAf + nBf > 0) {
+            const S* rec = a.Zr + ((int64_t)t * K + k) * (r + 1);
+            for (int c = tid; c < m; c += NT) zv[c] = ldcg(rec + c);
+            if (tid == 0) zv[MAXM] = ldcg(rec + r);
+            __syncthreads();
+            const S sig = zv[MAXM];
+            if (!is_zero(sig)) {
+                const int nrows = nAf + nBf;
+                for (int eb = tid / SPR; eb - tid / SPR < nrows; eb += NT / SPR) {
+                    const bool act = eb < nrows;
+                    const bool isA = eb < nAf;
+                    const int row = isA ? i4 + eb : i4 + (eb - nAf);
+                    S* gp = isA ? &IDX(a.A, a.lda, row, i1) : &IDX(a.B, a.ldb, row, i1);
+                    const int64_t ld = isA ? a.lda : a.ldb;
+                    S v[CPR];
+                    S s0 = S(0.0), s1 = S(0.0);
+                    if (act) {
+#pragma unroll
+                        for (int c = 0; c < CPR; ++c)
+                            if (c0 + c < m) {
+                                v[c] = ldcg(gp + (c0 + c) * ld);
+                                if (c & 1) s1 = fma_s(v[c], zv[c0 + c], s1);
+                                else s0 = fma_s(v[c], zv[c0 + c], s0);
+                            }
+                    }
+                    S sdot = s0 + s1;
+                    if constexpr (SPR > 1) {
+#pragma unroll
+                        for (int o = 1; o < SPR; o <<= 1) sdot += shfl_xor(sdot, o);
+                    }
+                    if (act) {
+                        const S sv = sdot * sig;
+#pragma unroll
+                        for (int c = 0; c < CPR; ++c)
+                            if (c0 + c < m) gp[(c0 + c) * ld] = v[c] - sv * conjv(zv[c0 + c]);
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        if (tid == 0) {
+            __threadfence();
+            st_release(&hprog[t], k + 1);
+        }
+    }
+}
+
 template <typename S, int NT, int MAXM>
 __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
     extern __shared__ __align__(16) unsigned char smraw[];
@@ -516,8 +605,14 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
     __shared__ int t_sh;
     if (threadIdx.x == 0) t_sh = atomicAdd(&a.prog[qp], 1);
     __syncthreads();
-    const int t = t_sh;
+    const bool helper = a.helpers && (t_sh & 1);
+    const int t = a.helpers ? (t_sh >> 1) : t_sh;
     if (t >= qp) return;
+    if (helper) {
+        far_strip_helper<S, NT, MAXM>(a, t, sm);
+        return;
+    }
+    int* hprog = a.prog + qp + 1;
     const int j = j1 + t;
     const int kcount = min(K, 2 + (n - j - 1) / r);
     const int kprev = (t > 0) ? min(K, 2 + (n - j) / r) : 0;
@@ -539,6 +634,14 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
                     }
                     (void)ld_acquire(&a.prog[t - 1]);
                 }
+                if (a.helpers) {  // far strip of (t-1, k+1) overlaps this step's rows >= b0(k-1)
+                    const int hneed = min(k + 2, kprev);
+                    if (ld_acquire(&hprog[t - 1]) < hneed) {
+                        while (ld_relaxed(&hprog[t - 1]) < hneed) {
+                        }
+                        (void)ld_acquire(&hprog[t - 1]);
+                    }
+                }
             }
             __syncthreads();
         }
@@ -547,7 +650,9 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
         const int i1 = j + k * r + 1;
         const int i2 = min(j + (k + 1) * r, n);
         const int i3 = min(j + (k + 2) * r, n);
-        const int i4 = j1 + 1 + max(0, (k + t - qp + 1) * r);
+        const int i4g = j1 + 1 + max(0, (k + t - qp + 1) * r);
+        // this CTA's part of the band: rows >= b0(k-1) when the helpers take the far rows
+        const int i4 = a.helpers ? max(i4g, j1 + (k - 1) * r + 1) : i4g;
         const int b0 = j1 + k * r + 1;
         const int m = i2 - i1 + 1;
         const int L = (t > 0) ? min(j - 1 + (k + 1) * r, n) - b0 + 1 : 0;

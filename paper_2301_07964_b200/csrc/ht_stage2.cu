@@ -165,10 +165,11 @@ struct Plan {
     // of Q and Z.  comm == nullptr: one GPU (emul > 1 splits the Q/Z chains into emulated slabs).
     ncclComm_t comm = nullptr;
     int rank = 0, nranks = 1, root = 0, emul = 1;
+    int helpers = 1;  // far-strip helper CTAs in the chase (2q CTAs)
     bool is_root() const { return comm == nullptr || rank == root; }
     bool qz() const { return Q || Z; }
     bool same(const Plan& o) const {
-        return n == o.n && r == o.r && q == o.q && strip_cap == o.strip_cap && H == o.H && ldh == o.ldh &&
+        return n == o.n && r == o.r && q == o.q && strip_cap == o.strip_cap && helpers == o.helpers && H == o.H && ldh == o.ldh &&
                T == o.T && ldt == o.ldt && Q == o.Q && ldq == o.ldq && Z == o.Z && ldz == o.ldz;
     }
 };
@@ -202,7 +203,7 @@ struct Workspace {
         CK(mal((void**)&Zr, rec));
         CK(mal((void**)&Qr, rec));
         CK(mal((void**)&Tr, tf));
-        CK(mal((void**)&prog, (size_t)(p.q + 1) * sizeof(int)));
+        CK(mal((void**)&prog, (size_t)(2 * p.q + 2) * sizeof(int)));
         if (k1p) {
             CK(mal((void**)&k1prof, 12 * sizeof(long long)));
             CK(cudaMemsetAsync(k1prof, 0, 12 * sizeof(long long), stream));
@@ -329,12 +330,13 @@ int enqueue_groups(const Plan<S>& p, Workspace<S>& ws, cudaStream_t stream, bool
         const bool root = p.is_root();
         if (prof) CK(cudaEventRecord(ev[5 * g + 0], stream));
         if (root) {
-            CK(cudaMemsetAsync(ws.prog, 0, (size_t)(q + 1) * sizeof(int), stream));
+            CK(cudaMemsetAsync(ws.prog, 0, (size_t)(2 * q + 2) * sizeof(int), stream));
             CK(cudaMemsetAsync(ws.Qr, 0, (size_t)qp * K * (r + 1) * sizeof(S), stream));
             CK(cudaMemsetAsync(ws.Zr, 0, (size_t)qp * K * (r + 1) * sizeof(S), stream));
-            ChaseArgs<S> ca{n, r, qp, j1, K, p.H, p.ldh, p.T, p.ldt, ws.Qr, ws.Zr, ws.Tr, TLD, ws.prog, p.strip_cap, ws.k1prof};
+            ChaseArgs<S> ca{n, r, qp, j1, K, p.H, p.ldh, p.T, p.ldt, ws.Qr, ws.Zr, ws.Tr, TLD, ws.prog, p.strip_cap,
+                            p.helpers, ws.k1prof};
             void* kargs[] = {&ca};
-            CK(cudaLaunchKernel(p.chase_fn, dim3(qp), dim3(CHASE_NT), kargs, p.chase_bytes, stream));
+            CK(cudaLaunchKernel(p.chase_fn, dim3(qp * (p.helpers ? 2 : 1)), dim3(CHASE_NT), kargs, p.chase_bytes, stream));
         }
         if (p.comm && qz) {  // the group's reflectors (2 qp K (r+1) scalars) from the root to every rank
             const size_t cnt = nccl_count<S>((size_t)qp * K * (r + 1));
@@ -545,8 +547,10 @@ int run(int64_t n64, int64_t r64, S* H, int64_t ldh, S* T, int64_t ldt, S* Q, in
     CK(cudaFuncSetAttribute(accum_kernel<S, ACC_NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)acc_bytes));
 
     if (int rcp = chain_prepare<S>(WP)) return rcp;
+    const int helpers = getenv("HT_NO_HELPERS") ? 0 : (2 * q <= nsm ? 1 : 0);
     Plan<S> pl{n, r, q, WP, LDB, Kmax, strip_cap, chase_bytes, acc_bytes, chase_fn, H, ldh, T, ldt, Q, ldq, Z, ldz,
-               std::max(8, nsm - q)};
+               std::max(8, nsm - (helpers ? 2 : 1) * q)};
+    pl.helpers = helpers;
     if (comm) {
         pl.comm = comm;
         NK(ncclCommCount(comm, &pl.nranks));
