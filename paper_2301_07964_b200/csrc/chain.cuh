@@ -164,7 +164,7 @@ __device__ __forceinline__ bool chain_tile(const ChainParams<S>& P, int bid, uns
         bid -= P.job[0].ntiles;
         jb_ = 1;
     }
-    const ChainJob<S> J = P.job[jb_];
+    const ChainJob<S> J = (jb_ == 0) ? P.job[0] : P.job[1];  // (no dynamic param indexing: no local memory)
     const int mode = J.mode;
     const bool trans = J.trans != 0;
     const int R0 = (J.tile0 + bid) * CH_BM + 1;  // first tile row (1-based)
@@ -355,11 +355,15 @@ __device__ __forceinline__ bool chain_tile(const ChainParams<S>& P, int bid, uns
             const int row = tid >> 2, part = tid & 3;  // 4 threads per row (CH_NT/4 >= CH_BM)
             const int g = R0 + row;
             const bool active = row < nr && g >= i5s && g <= rowmax(k);
-            for (int t = 1; t < qp; ++t) {
-                const int j = j1 + t;
-                const int i1 = j + k * r + 1, i2 = min(j + (k + 1) * r, n);
-                const int m = i2 - i1 + 1;
-                if (m < 2 || k >= min(K, 2 + (n - j - 1) / r)) continue;
+            // reflector t reaches rows <= i4a(t) = j1 + max(0,(k+t-qp+1)r): start at the first t
+            // reaching this tile's staircase rows (uniform); steps without a reflector have a zero
+            // record (sigma = 0)
+            const int lo = max(i5s, R0);
+            int t0 = 1;
+            if (j1 < lo) t0 = max(1, (lo - j1 + r - 1) / r - k + qp - 1);
+            for (int t = t0; t < qp; ++t) {
+                const int m = min(r, n - (j1 + t + k * r));
+                if (m < 2) continue;
                 const int i4a = j1 + max(0, (k + t - qp + 1) * r);
                 const S* zr = zsm + (size_t)t * (r + 1);
                 const S sig = zr[r];
@@ -399,8 +403,12 @@ __device__ __forceinline__ bool chain_tile(const ChainParams<S>& P, int bid, uns
 
 // Persistent over tiles: CTA b processes tiles b, b + gridDim.x, ... (a grid smaller than the
 // tile count leaves SMs free for the chase kernel running concurrently on another stream).
+// resident CTAs per SM the register budget targets (real: 3 x 256 threads; complex: 2)
 template <typename S, int WP>
-__global__ void __launch_bounds__(chain_nt(WP)) chain_kernel(ChainParams<S> P) {
+__host__ __device__ constexpr int chain_minb() { return (sizeof(S) == 8 && WP <= 128) ? 768 / chain_nt(WP) : 512 / chain_nt(WP); }
+
+template <typename S, int WP>
+__global__ void __launch_bounds__(chain_nt(WP), chain_minb<S, WP>()) chain_kernel(ChainParams<S> P) {
     extern __shared__ __align__(16) unsigned char smraw[];
     const int total = P.job[0].ntiles + (P.njobs > 1 ? P.job[1].ntiles : 0);
     uint64_t* bars = reinterpret_cast<uint64_t*>(smraw);

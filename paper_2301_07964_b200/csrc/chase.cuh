@@ -37,8 +37,10 @@ struct ChaseArgs {
     int* prog;  // prog[0..qp): steps completed by each sweep; prog[qp]: ticket;
                 // prog[qp+1 .. 2qp+1): far-strip items completed by each helper
     int strip_cap;  // strip rows (A then B) staged in shared memory per step
-    int helpers;    // 1: far strips (rows above b0(k-1)) go to one helper CTA per sweep
-    long long* prof;  // optional: per-CTA cycle counts of the step phases (8 slots)
+    int helpers;    // H >= 1: far strips (rows above b0(k-1)) go to H helper CTAs per sweep, which
+                    // own interleaved 64-row blocks of the matrix (hprog[t*H + h])
+    long long* prof;  // optional: per-CTA cycle counts of the step phases (12 slots)
+    int prof_t0;      // >= 0: only sweep prof_t0 of each group records
 };
 
 __device__ __forceinline__ int ld_acquire(const int* p) {
@@ -489,7 +491,9 @@ __host__ __device__ inline size_t chase_smem_elems(int r, int qp, int strip_cap)
 // and after helper t-1's item k+1 (lag as the sweeps).  Sweep t+1 waits for helper t before its
 // step k-1 (see chase_kernel).
 template <typename S, int NT, int MAXM>
-__device__ __forceinline__ void far_strip_helper(const ChaseArgs<S>& a, int t, S* sm) {
+__device__ __forceinline__ void far_strip_helper(const ChaseArgs<S>& a, int t, int h, S* sm) {
+    const int H = a.helpers;
+    constexpr int RB = 64;  // row block: helper h owns blocks h, h+H, ... (relative to j1)
     const int n = a.n, r = a.r, qp = a.qp, j1 = a.j1, K = a.K;
     const int j = j1 + t;
     const int kcount = min(K, 2 + (n - j - 1) / r);
@@ -507,11 +511,11 @@ __device__ __forceinline__ void far_strip_helper(const ChaseArgs<S>& a, int t, S
                 }
             if (t > 0) {
                 const int need = min(k + 2, kprev);
-                while (ld_relaxed(&hprog[t - 1]) < need) {
+                while (ld_relaxed(&hprog[(t - 1) * H + h]) < need) {
                 }
             }
             (void)ld_acquire(&a.prog[t]);
-            if (t > 0) (void)ld_acquire(&hprog[t - 1]);
+            if (t > 0) (void)ld_acquire(&hprog[(t - 1) * H + h]);
         }
         __syncthreads();
         const int i1 = j + k * r + 1;
@@ -528,34 +532,41 @@ __device__ __forceinline__ void far_strip_helper(const ChaseArgs<S>& a, int t, S
             __syncthreads();
             const S sig = zv[MAXM];
             if (!is_zero(sig)) {
-                const int nrows = nAf + nBf;
-                for (int eb = tid / SPR; eb - tid / SPR < nrows; eb += NT / SPR) {
-                    const bool act = eb < nrows;
-                    const bool isA = eb < nAf;
-                    const int row = isA ? i4 + eb : i4 + (eb - nAf);
-                    S* gp = isA ? &IDX(a.A, a.lda, row, i1) : &IDX(a.B, a.ldb, row, i1);
-                    const int64_t ld = isA ? a.lda : a.ldb;
-                    S v[CPR];
-                    S s0 = S(0.0), s1 = S(0.0);
-                    if (act) {
+                // my row blocks intersected with the far rows [i4, i4 + nAf) (A) and [i4, i4 + nBf) (B)
+                const int nfar = max(nAf, nBf);
+                const int blk0 = (i4 - j1) / RB, blk1 = (i4 + nfar - 1 - j1) / RB;
+                for (int blk = blk0 + ((h - blk0 % H) + H) % H; blk <= blk1; blk += H) {
+                    const int rlo = max(i4, j1 + blk * RB), rhi = min(i4 + nfar, j1 + (blk + 1) * RB);
+                    const int nrA = max(0, min(rhi, i4 + nAf) - rlo), nrB = max(0, min(rhi, i4 + nBf) - rlo);
+                    const int nrows = nrA + nrB;
+                    for (int eb = tid / SPR; eb - tid / SPR < nrows; eb += NT / SPR) {
+                        const bool act = eb < nrows;
+                        const bool isA = eb < nrA;
+                        const int row = isA ? rlo + eb : rlo + (eb - nrA);
+                        S* gp = isA ? &IDX(a.A, a.lda, row, i1) : &IDX(a.B, a.ldb, row, i1);
+                        const int64_t ld = isA ? a.lda : a.ldb;
+                        S v[CPR];
+                        S s0 = S(0.0), s1 = S(0.0);
+                        if (act) {
 #pragma unroll
-                        for (int c = 0; c < CPR; ++c)
-                            if (c0 + c < m) {
-                                v[c] = ldcg(gp + (c0 + c) * ld);
-                                if (c & 1) s1 = fma_s(v[c], zv[c0 + c], s1);
-                                else s0 = fma_s(v[c], zv[c0 + c], s0);
-                            }
-                    }
-                    S sdot = s0 + s1;
-                    if constexpr (SPR > 1) {
+                            for (int c = 0; c < CPR; ++c)
+                                if (c0 + c < m) {
+                                    v[c] = ldcg(gp + (c0 + c) * ld);
+                                    if (c & 1) s1 = fma_s(v[c], zv[c0 + c], s1);
+                                    else s0 = fma_s(v[c], zv[c0 + c], s0);
+                                }
+                        }
+                        S sdot = s0 + s1;
+                        if constexpr (SPR > 1) {
 #pragma unroll
-                        for (int o = 1; o < SPR; o <<= 1) sdot += shfl_xor(sdot, o);
-                    }
-                    if (act) {
-                        const S sv = sdot * sig;
+                            for (int o = 1; o < SPR; o <<= 1) sdot += shfl_xor(sdot, o);
+                        }
+                        if (act) {
+                            const S sv = sdot * sig;
 #pragma unroll
-                        for (int c = 0; c < CPR; ++c)
-                            if (c0 + c < m) gp[(c0 + c) * ld] = v[c] - sv * conjv(zv[c0 + c]);
+                            for (int c = 0; c < CPR; ++c)
+                                if (c0 + c < m) gp[(c0 + c) * ld] = v[c] - sv * conjv(zv[c0 + c]);
+                        }
                     }
                 }
             }
@@ -563,7 +574,7 @@ __device__ __forceinline__ void far_strip_helper(const ChaseArgs<S>& a, int t, S
         __syncthreads();
         if (tid == 0) {
             __threadfence();
-            st_release(&hprog[t], k + 1);
+            st_release(&hprog[t * H + h], k + 1);
         }
     }
 }
@@ -605,11 +616,11 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
     __shared__ int t_sh;
     if (threadIdx.x == 0) t_sh = atomicAdd(&a.prog[qp], 1);
     __syncthreads();
-    const bool helper = a.helpers && (t_sh & 1);
-    const int t = a.helpers ? (t_sh >> 1) : t_sh;
+    const int role = t_sh % (1 + a.helpers);  // tickets: sweep t, then its helpers
+    const int t = t_sh / (1 + a.helpers);
     if (t >= qp) return;
-    if (helper) {
-        far_strip_helper<S, NT, MAXM>(a, t, sm);
+    if (role > 0) {
+        far_strip_helper<S, NT, MAXM>(a, t, role - 1, sm);
         return;
     }
     int* hprog = a.prog + qp + 1;
@@ -634,14 +645,17 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
                     }
                     (void)ld_acquire(&a.prog[t - 1]);
                 }
-                if (a.helpers) {  // far strip of (t-1, k+1) overlaps this step's rows >= b0(k-1)
+                K1_TICK(0);
+                for (int h = 0; h < a.helpers; ++h) {  // far strip of (t-1, k+1) overlaps rows >= b0(k-1)
                     const int hneed = min(k + 2, kprev);
-                    if (ld_acquire(&hprog[t - 1]) < hneed) {
-                        while (ld_relaxed(&hprog[t - 1]) < hneed) {
+                    int* hp = &hprog[(t - 1) * a.helpers + h];
+                    if (ld_acquire(hp) < hneed) {
+                        while (ld_relaxed(hp) < hneed) {
                         }
-                        (void)ld_acquire(&hprog[t - 1]);
+                        (void)ld_acquire(hp);
                     }
                 }
+                K1_TICK(9);
             }
             __syncthreads();
         }
@@ -924,7 +938,7 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
         }
         cur ^= 1;
     }
-    if (a.prof && tid == 0)
+    if (a.prof && tid == 0 && (a.prof_t0 < 0 || t == a.prof_t0))
         for (int i = 0; i < 12; ++i) atomicAdd((unsigned long long*)&a.prof[i], (unsigned long long)pt[i]);
 #undef K1_TICK
 }

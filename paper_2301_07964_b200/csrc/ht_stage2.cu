@@ -203,7 +203,7 @@ struct Workspace {
         CK(mal((void**)&Zr, rec));
         CK(mal((void**)&Qr, rec));
         CK(mal((void**)&Tr, tf));
-        CK(mal((void**)&prog, (size_t)(2 * p.q + 2) * sizeof(int)));
+        CK(mal((void**)&prog, (size_t)(5 * p.q + 2) * sizeof(int)));
         if (k1p) {
             CK(mal((void**)&k1prof, 12 * sizeof(long long)));
             CK(cudaMemsetAsync(k1prof, 0, 12 * sizeof(long long), stream));
@@ -247,7 +247,7 @@ struct Workspace {
 };
 
 void print_k1prof(const long long* h) {
-    const char* nm[12] = {"wait", "loads", "catchup", "QB+T", "larfgZ", "strip", "RQ", "larfgQ", "writes", "s9", "s10", "s11"};
+    const char* nm[12] = {"wait", "loads", "catchup", "QB+T", "larfgZ", "strip", "RQ", "larfgQ", "writes", "waitH", "s10", "s11"};
     double tot = 0;
     for (int i = 0; i < 12; ++i) tot += (double)h[i];
     fprintf(stderr, "K1 cycles (sum over CTAs):");
@@ -330,13 +330,13 @@ int enqueue_groups(const Plan<S>& p, Workspace<S>& ws, cudaStream_t stream, bool
         const bool root = p.is_root();
         if (prof) CK(cudaEventRecord(ev[5 * g + 0], stream));
         if (root) {
-            CK(cudaMemsetAsync(ws.prog, 0, (size_t)(2 * q + 2) * sizeof(int), stream));
+            CK(cudaMemsetAsync(ws.prog, 0, (size_t)((1 + p.helpers) * q + 1) * sizeof(int), stream));
             CK(cudaMemsetAsync(ws.Qr, 0, (size_t)qp * K * (r + 1) * sizeof(S), stream));
             CK(cudaMemsetAsync(ws.Zr, 0, (size_t)qp * K * (r + 1) * sizeof(S), stream));
             ChaseArgs<S> ca{n, r, qp, j1, K, p.H, p.ldh, p.T, p.ldt, ws.Qr, ws.Zr, ws.Tr, TLD, ws.prog, p.strip_cap,
-                            p.helpers, ws.k1prof};
+                            p.helpers, ws.k1prof, getenv("HT_K1PROF_T") ? atoi(getenv("HT_K1PROF_T")) : -1};
             void* kargs[] = {&ca};
-            CK(cudaLaunchKernel(p.chase_fn, dim3(qp * (p.helpers ? 2 : 1)), dim3(CHASE_NT), kargs, p.chase_bytes, stream));
+            CK(cudaLaunchKernel(p.chase_fn, dim3(qp * (1 + p.helpers)), dim3(CHASE_NT), kargs, p.chase_bytes, stream));
         }
         if (p.comm && qz) {  // the group's reflectors (2 qp K (r+1) scalars) from the root to every rank
             const size_t cnt = nccl_count<S>((size_t)qp * K * (r + 1));
@@ -547,9 +547,12 @@ int run(int64_t n64, int64_t r64, S* H, int64_t ldh, S* T, int64_t ldt, S* Q, in
     CK(cudaFuncSetAttribute(accum_kernel<S, ACC_NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)acc_bytes));
 
     if (int rcp = chain_prepare<S>(WP)) return rcp;
-    const int helpers = getenv("HT_NO_HELPERS") ? 0 : (2 * q <= nsm ? 1 : 0);
+    // far-strip helpers per sweep: as many as fit next to the q sweeps, at most 3 (HT_HELPERS)
+    int helpers = std::max(0, std::min(3, nsm / q - 2));  // q=32: 2, q<=21: 3
+    if (getenv("HT_HELPERS")) helpers = std::max(0, std::min(3, atoi(getenv("HT_HELPERS"))));
+    if (getenv("HT_NO_HELPERS") || (1 + helpers) * q > nsm) helpers = 0;
     Plan<S> pl{n, r, q, WP, LDB, Kmax, strip_cap, chase_bytes, acc_bytes, chase_fn, H, ldh, T, ldt, Q, ldq, Z, ldz,
-               std::max(8, nsm - (helpers ? 2 : 1) * q)};
+               std::max(8, nsm - (1 + helpers) * q)};
     pl.helpers = helpers;
     if (comm) {
         pl.comm = comm;
