@@ -73,3 +73,98 @@ __global__ void __launch_bounds__(NT) accum_kernel(AccumArgs<S> a) {
         Out[e] = (l < wk && c < wk) ? X[(size_t)l * LX + c] : S(0.0);
     }
 }
+
+// ---------------------------------------------------------------------------------------
+// K2m: merged window blocks for the apply chains.  Consecutive windows overlap in q-1 columns,
+// so P of them (k = klo .. khi) act on W = q + P r - 1 columns and, applied in the chain's
+// descending order, compose to ONE W x W block
+//     M = V'_khi V'_{khi-1} ... V'_klo      (V'_k = V_k embedded at column offset (k-klo) r),
+// the same for U.  A merged chain step costs W^2 per row against P w^2 for P single steps
+// (about equal for P ~ 4 at q ~ 2r) but syncs and streams once instead of P times.
+// Grid (ceil(K/P), 2); group mg covers windows [mg P, min(K-1, mg P + P - 1)].  Real fp64 only.
+template <typename S>
+struct MergeArgs {
+    int n, r, qp, j1, K, P, WP, LDB;
+    const S* U;  // single blocks (chain layout: WP x LDB row-major, zero padded)
+    const S* V;
+    S* MU;       // merged blocks, same layout
+    S* MV;
+};
+
+template <typename S>
+__host__ __device__ inline size_t merge_smem_bytes(int W, int w) {
+    return (2 * (size_t)W * (W | 1) + (size_t)w * (w | 1)) * sizeof(S);
+}
+
+template <typename S, int NT>
+__global__ void __launch_bounds__(NT) merge_kernel(MergeArgs<S> a) {
+    extern __shared__ __align__(16) unsigned char smraw[];
+    const int n = a.n, r = a.r, qp = a.qp, j1 = a.j1, K = a.K, P = a.P;
+    const int mg = blockIdx.x;
+    const bool isV = blockIdx.y != 0;
+    const S* Blk = isV ? a.V : a.U;
+    S* Out = (isV ? a.MV : a.MU) + (size_t)mg * a.WP * a.LDB;
+    const int w = qp + r - 1;
+    const int klo = mg * P, khi = min(K - 1, klo + P - 1);
+    const int c0 = j1 + klo * r + 1;
+    const int W = min(qp + (khi - klo + 1) * r - 1, n - c0 + 1);
+    const int LM = W | 1;
+    S* M = reinterpret_cast<S*>(smraw);
+    S* M2 = M + (size_t)W * LM;
+    S* Vs = M2 + (size_t)W * LM;  // the current window block (w x (w|1))
+    const int LV = w | 1;
+    const int tid = threadIdx.x;
+    // M = V'_khi (identity outside its columns)
+    {
+        const int o = (khi - klo) * r;
+        const int wk = min(w, n - (j1 + khi * r + 1) + 1);
+        const S* B = Blk + (size_t)khi * a.WP * a.LDB;
+        for (int e = tid; e < W * LM; e += NT) {
+            const int l = e / LM, c = e % LM;
+            S v = S(0.0);
+            if (c < W) {
+                if (l >= o && l < o + wk && c >= o && c < o + wk) v = B[(size_t)(l - o) * a.LDB + (c - o)];
+                else if (l == c) v = S(1.0);
+            }
+            M[e] = v;
+        }
+    }
+    __syncthreads();
+    for (int k = khi - 1; k >= klo; --k) {  // M <- M V'_k (columns o .. o+wk)
+        const int o = (k - klo) * r;
+        const int wk = min(w, n - (j1 + k * r + 1) + 1);
+        const S* B = Blk + (size_t)k * a.WP * a.LDB;
+        for (int e = tid; e < wk * wk; e += NT) {
+            const int l = e / wk, c = e % wk;
+            Vs[(size_t)l * LV + c] = B[(size_t)l * a.LDB + c];
+        }
+        __syncthreads();
+        for (int e = tid; e < W * LM; e += NT) {
+            const int l = e / LM, c = e % LM;
+            S v = M[e];
+            if (c >= o && c < o + wk) {
+                S s0 = S(0.0), s1 = S(0.0), s2 = S(0.0), s3 = S(0.0);
+                const S* mr = M + (size_t)l * LM + o;
+                const S* vc = Vs + (c - o);
+                int cc = 0;
+                for (; cc + 3 < wk; cc += 4) {
+                    s0 = fma_s(mr[cc], vc[(size_t)cc * LV], s0);
+                    s1 = fma_s(mr[cc + 1], vc[(size_t)(cc + 1) * LV], s1);
+                    s2 = fma_s(mr[cc + 2], vc[(size_t)(cc + 2) * LV], s2);
+                    s3 = fma_s(mr[cc + 3], vc[(size_t)(cc + 3) * LV], s3);
+                }
+                for (; cc < wk; ++cc) s0 = fma_s(mr[cc], vc[(size_t)cc * LV], s0);
+                v = (s0 + s1) + (s2 + s3);
+            }
+            M2[e] = v;
+        }
+        __syncthreads();
+        S* tmp = M;
+        M = M2;
+        M2 = tmp;
+    }
+    for (int e = tid; e < a.WP * a.LDB; e += NT) {
+        const int l = e / a.LDB, c = e % a.LDB;
+        Out[e] = (l < W && c < W) ? M[(size_t)l * LM + c] : S(0.0);
+    }
+}

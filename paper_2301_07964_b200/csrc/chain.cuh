@@ -31,6 +31,7 @@ struct ChainJob {
     S* M;
     int64_t ld;
     const S* Blk;  // K blocks, each WP rows x LDB (row-major, padded rows/cols zero)
+    const S* MBlk; // merged blocks (P > 1): ceil(K/P) blocks of P consecutive windows, same layout
     int mode;
     int trans;
     int ntiles;
@@ -43,6 +44,7 @@ struct ChainParams {
     ChainJob<S> job[2];
     int njobs;
     const S* Zr;  // staircase reflectors: (qp*K) records of (r+1)
+    int P;        // window merge factor (1 = off): steps cover P windows where the tile is fully inside
 };
 
 constexpr int CH_BM = 32;      // tile rows per CTA (one warp row of 4 m8 tiles)
@@ -57,8 +59,8 @@ __host__ __device__ constexpr int chain_nt(int WP) { return 32 * chain_wn(WP); }
 
 // dynamic smem: [64 B mbarriers][circular X: (w+r) x CH_LDX][block ring][staircase refl.]
 template <typename S, int WP>
-__host__ __device__ constexpr size_t chain_smem_bytes(int r, int q) {
-    return 64 + (size_t)(q + r - 1 + r) * CH_LDX * sizeof(S) +
+__host__ __device__ constexpr size_t chain_smem_bytes(int r, int q, int P = 1) {
+    return 64 + (size_t)(P > 1 ? q + 2 * P * r - 1 : q + r - 1 + r) * CH_LDX * sizeof(S) +
            (size_t)CH_STAGES * CH_KC * chain_ldb(WP) * sizeof(S) + (size_t)(q + 1) * (r + 1) * sizeof(S);
 }
 
@@ -156,7 +158,8 @@ __device__ __forceinline__ bool chain_tile(const ChainParams<S>& P, int bid, uns
     static_assert(WP % (8 * WN) == 0, "window padding");
     const int n = P.n, r = P.r, qp = P.qp, j1 = P.j1, K = P.K;
     const int w = qp + r - 1;
-    const int CIRC = w + r;  // circular buffer columns
+    const int PM = P.P;
+    const int CIRC = PM > 1 ? qp + 2 * PM * r - 1 : w + r;  // circular buffer columns
 
     // ---- which job / tile ----
     int jb_ = 0;
@@ -194,6 +197,22 @@ __device__ __forceinline__ bool chain_tile(const ChainParams<S>& P, int bid, uns
     }
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int wn = warp;
+    // ---- step sequence: from window khi downward, a step covers windows [klo, khi]: a whole
+    // merge group [mg P, mg P + P - 1] when khi is its top and the tile is fully inside every
+    // window of it (no staircase / column limit), else the single window khi ----
+    auto step_lo = [&](int khi) -> int {
+        if (PM <= 1) return khi;
+        const int glo = (khi / PM) * PM;
+        if (khi != min(K - 1, glo + PM - 1) || glo < kend) return khi;
+        bool full = true;
+        if (mode == CM_AB_RIGHT) full = R1 <= j1 + max(0, (glo - qp + 1) * r);
+        else if (mode == CM_A_LEFT || mode == CM_B_LEFT) full = R0 > cstart(khi);
+        return full ? glo : khi;
+    };
+    auto step_blk = [&](int khi, int klo) -> const S* {
+        return klo < khi ? J.MBlk + ((size_t)(klo / PM) * WP) * LDB : J.Blk + ((size_t)khi * WP) * LDB;
+    };
+    auto step_w = [&](int khi, int klo) { return min(qp + (khi - klo + 1) * r - 1, n - (j1 + klo * r + 1) + 1); };
 
     // zero the circular buffer (padded K rows of the blocks are zero; keep X finite)
     for (int e = tid; e < CIRC * CH_LDX; e += CH_NT) X[e] = S(0.0);
@@ -242,50 +261,52 @@ __device__ __forceinline__ bool chain_tile(const ChainParams<S>& P, int bid, uns
         }
     };
 
-    // ---- block ring producer (thread 0): chunk sequence over (window, chunk) ----
-    int pk = kstart, pc = 0;  // next chunk to issue
+    // ---- block ring producer (thread 0): chunk sequence over (step, chunk) ----
+    int pk = kstart, pc = 0;  // top window of the step being issued, next chunk of it
+    int pklo = step_lo(kstart);
     unsigned pseq = 0;
-    auto nchunks = [&](int k) {
-        const int wk = min(w, n - (j1 + k * r + 1) + 1);
-        return (wk + CH_KC - 1) / CH_KC;
-    };
     auto issue_next = [&]() {
         if (tid != 0 || pk < kend) return;
         const int s = pseq % CH_STAGES;
-        const S* src = J.Blk + ((size_t)pk * WP + (size_t)pc * CH_KC) * LDB;
+        const S* src = step_blk(pk, pklo) + (size_t)pc * CH_KC * LDB;
         mbar_expect_tx(&bars[s], CH_KC * LDB * sizeof(S));
         bulk_g2s(ring + (size_t)s * CH_KC * LDB, src, CH_KC * LDB * sizeof(S), &bars[s]);
         ++pseq;
-        if (++pc == nchunks(pk)) {
+        if (++pc == (step_w(pk, pklo) + CH_KC - 1) / CH_KC) {
             pc = 0;
-            --pk;
+            pk = pklo - 1;
+            if (pk >= kend) pklo = step_lo(pk);
         }
     };
     for (int s = 0; s < CH_STAGES - 1; ++s) issue_next();
 
-    // first window: all of its columns
-    int p = 0;  // circular position of the current window's first column
+    // first step: all of its columns
+    int p = 0;  // circular position of the current step's first column
     {
-        const int c0 = j1 + kstart * r + 1;
-        load_cols(c0, min(w, n - c0 + 1), 0);
+        const int klo0 = step_lo(kstart);
+        const int c0 = j1 + klo0 * r + 1;
+        load_cols(c0, step_w(kstart, klo0), 0);
         cp_async_commit();
     }
     unsigned cseq = 0;  // consumer chunk sequence
-    for (int k = kstart; k >= kend; --k) {
-        const int c0 = j1 + k * r + 1;
-        const int wk = min(w, n - c0 + 1);
-        const bool has_next = k - 1 >= kend;
-        const int cn = has_next ? min(qp - 1, wk) : 0;  // carried into window k-1
+    for (int k = kstart, klo = step_lo(kstart); k >= kend;) {
+        const bool merged = klo < k;
+        const int c0 = j1 + klo * r + 1;
+        const int wk = step_w(k, klo);
+        const bool has_next = klo - 1 >= kend;
+        const int nklo = has_next ? step_lo(klo - 1) : 0;
+        const int shift = has_next ? (klo - nklo) * r : 0;  // fresh columns of the next step
+        const int cn = has_next ? min(qp - 1, wk) : 0;      // carried into the next step
         cp_async_wait_all();
         __syncthreads();
-        // prefetch: fresh columns of window k-1 and (H/T right) window k's staircase reflectors
+        // prefetch: fresh columns of the next step and (H/T right) this window's staircase reflectors
         if (has_next) {
-            int pn = p - r;
+            int pn = p - shift;
             if (pn < 0) pn += CIRC;
-            load_cols(c0 - r, r, pn);
+            load_cols(c0 - shift, shift, pn);
         }
         const int i5s = j1 + 1 + max(0, (k - qp + 1) * r);
-        const bool stair = mode == CM_AB_RIGHT && qp >= 2 && max(i5s, R0) <= min(rowmax(k), R1);
+        const bool stair = !merged && mode == CM_AB_RIGHT && qp >= 2 && max(i5s, R0) <= min(rowmax(k), R1);
         if (stair) {
             const S* src = P.Zr + (size_t)k * (r + 1);
             for (int t = 1 + warp; t < qp; t += NW)
@@ -321,17 +342,19 @@ __device__ __forceinline__ bool chain_tile(const ChainParams<S>& P, int bid, uns
 #pragma unroll
                 for (int nt = 0; nt < NTL; ++nt)
                     b[nt] = maybe_conj(Bs[(kk + (lane & 3)) * LDB + colb + nt * 8], trans);
+                if (wn * (WP / WN) < wk) {  // warp-uniform: this warp's columns exist in the step
 #pragma unroll
-                for (int mt = 0; mt < MT; ++mt)
+                    for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
-                    for (int nt = 0; nt < NTL; ++nt) mma_step(acc[mt][nt], a[mt], b[nt]);
+                        for (int nt = 0; nt < NTL; ++nt) mma_step(acc[mt][nt], a[mt], b[nt]);
+                }
             }
             ++cseq;
         }
         __syncthreads();  // all reads of X done
         // ---- epilogue: write Y back in place for the rows the mode updates ----
-        const int ylo = (mode == CM_A_LEFT || mode == CM_B_LEFT) ? cstart(k) : 0;
-        const int yhi = (mode == CM_AB_RIGHT) ? j1 + max(0, (k - qp + 1) * r) : 0x7fffffff;
+        const int ylo = (!merged && (mode == CM_A_LEFT || mode == CM_B_LEFT)) ? cstart(k) : 0;
+        const int yhi = (!merged && mode == CM_AB_RIGHT) ? j1 + max(0, (k - qp + 1) * r) : 0x7fffffff;
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt) {
             const int row = rowb + mt * 8;
@@ -394,8 +417,10 @@ __device__ __forceinline__ bool chain_tile(const ChainParams<S>& P, int bid, uns
             if (po >= CIRC) po -= CIRC;
             store_cols(c0 + cn, wk - cn, po);
         }
-        p -= r;
+        p -= shift;
         if (p < 0) p += CIRC;
+        k = klo - 1;
+        klo = nklo;
     }
     cp_async_wait_all();
     return true;

@@ -53,11 +53,11 @@ int64_t default_q(int64_t n, int64_t r, int is_complex) {
 }
 
 template <typename S, int WP>
-size_t chain_bytes(int r, int q) { return chain_smem_bytes<S, WP>(r, q); }
+size_t chain_bytes(int r, int q, int P = 1) { return chain_smem_bytes<S, WP>(r, q, P); }
 
 template <typename S, int WP>
 int launch_chain(const ChainParams<S>& P, int grid, int r, int q, cudaStream_t st, size_t min_smem) {
-    const size_t bytes = std::max(chain_bytes<S, WP>(r, q), min_smem);
+    const size_t bytes = std::max(chain_bytes<S, WP>(r, q, P.P), min_smem);
     static bool attr_set = false;  // per instantiation
     if (!attr_set) {
         CK(cudaFuncSetAttribute(chain_kernel<S, WP>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
@@ -98,13 +98,13 @@ int chain_prepare(int WP) {  // smem attribute outside any stream capture
 }
 
 template <typename S>
-size_t chain_bytes_rt(int WP, int r, int q) {
+size_t chain_bytes_rt(int WP, int r, int q, int P = 1) {
     switch (WP) {
-        case 32: return chain_bytes<S, 32>(r, q);
-        case 64: return chain_bytes<S, 64>(r, q);
-        case 96: return chain_bytes<S, 96>(r, q);
-        case 128: return chain_bytes<S, 128>(r, q);
-        case 160: return chain_bytes<S, 160>(r, q);
+        case 32: return chain_bytes<S, 32>(r, q, P);
+        case 64: return chain_bytes<S, 64>(r, q, P);
+        case 96: return chain_bytes<S, 96>(r, q, P);
+        case 128: return chain_bytes<S, 128>(r, q, P);
+        case 160: return chain_bytes<S, 160>(r, q, P);
         default: return (size_t)1 << 40;
     }
 }
@@ -165,11 +165,13 @@ struct Plan {
     // of Q and Z.  comm == nullptr: one GPU (emul > 1 splits the Q/Z chains into emulated slabs).
     ncclComm_t comm = nullptr;
     int rank = 0, nranks = 1, root = 0, emul = 1;
-    int helpers = 1;  // far-strip helper CTAs in the chase (2q CTAs)
+    int helpers = 1;  // far-strip helper CTAs per sweep in the chase
+    int P = 1;        // window merge factor of the apply chains (K2m)
+    size_t mrg_bytes = 0;
     bool is_root() const { return comm == nullptr || rank == root; }
     bool qz() const { return Q || Z; }
     bool same(const Plan& o) const {
-        return n == o.n && r == o.r && q == o.q && strip_cap == o.strip_cap && helpers == o.helpers && H == o.H && ldh == o.ldh &&
+        return n == o.n && r == o.r && q == o.q && strip_cap == o.strip_cap && helpers == o.helpers && P == o.P && H == o.H && ldh == o.ldh &&
                T == o.T && ldt == o.ldt && Q == o.Q && ldq == o.ldq && Z == o.Z && ldz == o.ldz;
     }
 };
@@ -180,7 +182,7 @@ struct Plan {
 constexpr int NUV = 4;
 template <typename S>
 struct Workspace {
-    S *U[NUV] = {}, *V[NUV] = {}, *Zr = nullptr, *Qr = nullptr, *Tr = nullptr;
+    S *U[NUV] = {}, *V[NUV] = {}, *MU[NUV] = {}, *MV[NUV] = {}, *Zr = nullptr, *Qr = nullptr, *Tr = nullptr;
     int* prog = nullptr;
     long long* k1prof = nullptr;
     long long k1prof_host[12] = {0};
@@ -196,9 +198,14 @@ struct Workspace {
         auto mal = [&](void** ptr, size_t bytes) -> cudaError_t {
             return async ? cudaMallocAsync(ptr, bytes, stream) : cudaMalloc(ptr, bytes);
         };
+        const size_t mblk = (size_t)((p.Kmax + p.P - 1) / p.P) * p.WP * p.LDB * sizeof(S);
         for (int b = 0; b < (p.qz() ? NUV : 1); ++b) {
             CK(mal((void**)&U[b], blk));
             CK(mal((void**)&V[b], blk));
+            if (p.P > 1) {
+                CK(mal((void**)&MU[b], mblk));
+                CK(mal((void**)&MV[b], mblk));
+            }
         }
         CK(mal((void**)&Zr, rec));
         CK(mal((void**)&Qr, rec));
@@ -231,6 +238,8 @@ struct Workspace {
         for (int b = 0; b < NUV; ++b) {
             CK(fr(U[b]));
             CK(fr(V[b]));
+            CK(fr(MU[b]));
+            CK(fr(MV[b]));
         }
         CK(fr(Zr));
         CK(fr(Qr));
@@ -351,17 +360,23 @@ int enqueue_groups(const Plan<S>& p, Workspace<S>& ws, cudaStream_t stream, bool
             accum_kernel<S, ACC_NT><<<dim3(K, 2), ACC_NT, p.acc_bytes, stream>>>(aa);
             CK(cudaGetLastError());
             g_last_launches += 2;
+            if (p.P > 1) {
+                MergeArgs<S> ma{n, r, qp, j1, K, p.P, WP, LDB, ws.U[bsel], ws.V[bsel], ws.MU[bsel], ws.MV[bsel]};
+                merge_kernel<S, ACC_NT><<<dim3((K + p.P - 1) / p.P, 2), ACC_NT, p.mrg_bytes, stream>>>(ma);
+                CK(cudaGetLastError());
+                ++g_last_launches;
+            }
         }
         if (qz) CK(cudaEventRecord(ws.ev_uv[bsel], stream));
         if (prof) CK(cudaEventRecord(ev[5 * g + 1], stream));
         // ---- apply phase: right updates of H, T (staircase + V_k), then left (U_k^*) ----
         const int tiles = (n + CH_BM - 1) / CH_BM;
         if (root) {
-            ChainParams<S> pr{n, r, qp, j1, K, {{p.H, p.ldh, ws.V[bsel], CM_AB_RIGHT, 0, tiles, 0},
-                                                {p.T, p.ldt, ws.V[bsel], CM_AB_RIGHT, 0, tiles, 0}}, 2, ws.Zr};
+            ChainParams<S> pr{n, r, qp, j1, K, {{p.H, p.ldh, ws.V[bsel], ws.MV[bsel], CM_AB_RIGHT, 0, tiles, 0},
+                                                {p.T, p.ldt, ws.V[bsel], ws.MV[bsel], CM_AB_RIGHT, 0, tiles, 0}}, 2, ws.Zr, p.P};
             if (int rc = chain<S>(pr, WP, 2 * tiles, r, q, stream)) return rc;
-            ChainParams<S> pl{n, r, qp, j1, K, {{p.H, p.ldh, ws.U[bsel], CM_A_LEFT, 1, tiles, 0},
-                                                {p.T, p.ldt, ws.U[bsel], CM_B_LEFT, 1, tiles, 0}}, 2, ws.Zr};
+            ChainParams<S> pl{n, r, qp, j1, K, {{p.H, p.ldh, ws.U[bsel], ws.MU[bsel], CM_A_LEFT, 1, tiles, 0},
+                                                {p.T, p.ldt, ws.U[bsel], ws.MU[bsel], CM_B_LEFT, 1, tiles, 0}}, 2, ws.Zr, p.P};
             if (int rc = chain<S>(pl, WP, 2 * tiles, r, q, stream)) return rc;
             g_last_launches += 2;
         }
@@ -376,9 +391,10 @@ int enqueue_groups(const Plan<S>& p, Workspace<S>& ws, cudaStream_t stream, bool
                 if (p.comm) slab_tiles(n, p.nranks, p.rank, &t0, &nt);
                 else if (nslab > 1) slab_tiles(n, nslab, sl, &t0, &nt);
                 if (nt <= 0) continue;
-                ChainParams<S> pq{n, r, qp, j1, K, {{p.Q ? p.Q : p.Z, p.Q ? p.ldq : p.ldz, p.Q ? ws.U[bsel] : ws.V[bsel], CM_PLAIN, 0, nt, t0},
-                                                    {p.Z, p.ldz, ws.V[bsel], CM_PLAIN, 0, nt, t0}},
-                                  (p.Q && p.Z) ? 2 : 1, ws.Zr};
+                ChainParams<S> pq{n, r, qp, j1, K, {{p.Q ? p.Q : p.Z, p.Q ? p.ldq : p.ldz, p.Q ? ws.U[bsel] : ws.V[bsel],
+                                                     p.Q ? ws.MU[bsel] : ws.MV[bsel], CM_PLAIN, 0, nt, t0},
+                                                    {p.Z, p.ldz, ws.V[bsel], ws.MV[bsel], CM_PLAIN, 0, nt, t0}},
+                                  (p.Q && p.Z) ? 2 : 1, ws.Zr, p.P};
                 // persistent grid leaving q whole SMs: the chase of the next group starts at once
                 if (int rc = chain<S>(pq, WP, std::min(pq.njobs * nt, p.qz_ctas), r, q, ws.side, 116 * 1024)) return rc;
                 ++g_last_launches;
@@ -525,7 +541,20 @@ int run(int64_t n64, int64_t r64, S* H, int64_t ldh, S* T, int64_t ldt, S* Q, in
     int64_t q64 = (opts && opts->q > 0) ? opts->q : default_q(n, r, is_complex);
     const int q = (int)std::max<int64_t>(1, std::min<int64_t>(q64, n - 2));
     const int w = q + r - 1;
-    const int WP = (w + 31) / 32 * 32;  // padded window order (DMMA tiles, ring chunks)
+    // window merge factor of the apply chains: the largest P <= 4 whose merged order
+    // W = q + P r - 1 fits K2m's shared memory (W <= 96) and executes at most 15% more flops
+    // than P single windows (W^2 <= 1.15 P w^2); real fp64 only (HT_MERGE=0 disables)
+    int PM = 1;
+    if (sizeof(S) == 8 && !(getenv("HT_MERGE") && atoi(getenv("HT_MERGE")) == 0))
+        for (int P = 4; P >= 2; --P) {
+            const double Wd = q + P * r - 1.0;
+            if (Wd <= 96 && Wd * Wd <= 1.15 * P * (double)w * w) {
+                PM = P;
+                break;
+            }
+        }
+    const int Wm = q + PM * r - 1;
+    const int WP = (Wm + 31) / 32 * 32;  // padded window order (DMMA tiles, ring chunks)
     const int LDB = chain_ldb(WP);
     const int Kmax = 1 + (n - 1 - 2) / r;
     const int chase_budget = 200 * 1024;
@@ -536,13 +565,16 @@ int run(int64_t n64, int64_t r64, S* H, int64_t ldh, S* T, int64_t ldt, S* Q, in
     const size_t acc_bytes = accum_smem_bytes<S>(r, q);
     const void* chase_fn = chase_kernel_for<S>(r);
     if (!chase_fn || q > 148) return HT_EUNSUPPORTED;  // one co-resident CTA per sweep
-    const size_t ch_bytes = chain_bytes_rt<S>(WP, r, q);
+    const size_t ch_bytes = chain_bytes_rt<S>(WP, r, q, PM);
+    const size_t mrg_bytes = PM > 1 ? merge_smem_bytes<S>(Wm, w) : 0;
     int dev = 0, smem_optin = 0, nsm = 0;
     CK(cudaGetDevice(&dev));
     CK(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
     CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-    if (chase_bytes > (size_t)smem_optin || ch_bytes > (size_t)smem_optin || acc_bytes > (size_t)smem_optin)
+    if (chase_bytes > (size_t)smem_optin || ch_bytes > (size_t)smem_optin || acc_bytes > (size_t)smem_optin ||
+        mrg_bytes > (size_t)smem_optin)
         return HT_EUNSUPPORTED;
+    if (PM > 1) CK(cudaFuncSetAttribute(merge_kernel<S, ACC_NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mrg_bytes));
     CK(cudaFuncSetAttribute(chase_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)chase_bytes));
     CK(cudaFuncSetAttribute(accum_kernel<S, ACC_NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)acc_bytes));
 
@@ -554,6 +586,8 @@ int run(int64_t n64, int64_t r64, S* H, int64_t ldh, S* T, int64_t ldt, S* Q, in
     Plan<S> pl{n, r, q, WP, LDB, Kmax, strip_cap, chase_bytes, acc_bytes, chase_fn, H, ldh, T, ldt, Q, ldq, Z, ldz,
                std::max(8, nsm - (1 + helpers) * q)};
     pl.helpers = helpers;
+    pl.P = PM;
+    pl.mrg_bytes = mrg_bytes;
     if (comm) {
         pl.comm = comm;
         NK(ncclCommCount(comm, &pl.nranks));
