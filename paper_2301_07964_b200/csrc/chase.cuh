@@ -468,6 +468,10 @@ __device__ __forceinline__ void rq_dir(int m, const S* Cb, int LDC, S* ring, vol
     else rq_direction<S, MAXM>(m, Cb, LDC, ring, flag, uu);
 }
 
+// RQ ring slot length for the reflector length r (RQCfg<S,MAXM>::PLD of the MAXM that r uses;
+// >= r + 4 also covers the unrolled variant's MAXM + 4)
+__host__ __device__ inline int ring_pld(int r) { return r <= 32 ? r + 20 : (r <= 64 ? 68 : 132); }
+
 template <typename S>
 __host__ __device__ inline size_t chase_smem_elems(int r, int qp, int strip_cap) {
     const int w = qp + r - 1;
@@ -476,11 +480,12 @@ __host__ __device__ inline size_t chase_smem_elems(int r, int qp, int strip_cap)
     return 3 * XL +                      // x (2 buffers), y
            (overlay ? (size_t)r * 132 : (size_t)r * (r + 1)) +  // B block (| RQ ring)
            3 * (size_t)(r + 8) +         // vq, vz, uu
-           (overlay ? 0 : (size_t)r * (r + 20)) +  // RQ ring (pivot rows + scalars per stage)
+           (overlay ? 0 : (size_t)r * ring_pld(r)) +  // RQ ring (pivot rows + scalars per stage)
            16 +                          // scalars
            (size_t)qp * (r + 1) +        // catch-up records (Y)
            (size_t)qp * (qp + 1) +       // T factor of window k
            5 * (size_t)(qp + 8) +        // WY temporaries
+           (overlay ? 0 : XL + (size_t)r * (r + 1) + (size_t)qp * (r + 1) + (size_t)qp * (qp + 1)) +  // prefetch set
            (size_t)strip_cap * (r + 1);  // staged strip rows
 }
 
@@ -591,25 +596,31 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
     const int XL = w + r + 8;
     const int TL = qp + 1;
     S* xc[2] = {sm, sm + XL};  // column jb of this step / of the next step
-    S* ys = sm + 2 * XL;
+    S* ys0 = sm + 2 * XL;
     constexpr bool OVERLAY = MAXM > 64;  // RQ ring overlays Cb (the block goes to HBM after Q^*)
-    S* Cb = ys + XL;           // r x (r+1) col-major
+    constexpr bool PF = !OVERLAY;        // next step's B block / records / T / y prefetched during the RQ
+    S* Cb0 = ys0 + XL;         // r x (r+1) col-major
     static_assert(!OVERLAY || RQCfg<S, MAXM>::PLD <= 132, "ring slot of the overlay");
-    S* vq = Cb + (OVERLAY ? (size_t)r * 132 : (size_t)r * (r + 1));
+    S* vq = Cb0 + (OVERLAY ? (size_t)r * 132 : (size_t)r * (r + 1));
     S* vz = vq + (r + 8);
     S* uu = vz + (r + 8);
-    S* ring = OVERLAY ? Cb : uu + (r + 8);  // RQ ring: r x (r+20) (overlay: r x 132)
-    S* scal = uu + (r + 8) + (OVERLAY ? 0 : (size_t)r * (r + 20));
+    S* ring = OVERLAY ? Cb0 : uu + (r + 8);  // RQ ring: r x ring_pld(r) (overlay: r x 132)
+    static_assert(OVERLAY || RQCfg<S, MAXM>::PLD <= 68 || MAXM <= 32, "ring slot");
+    S* scal = uu + (r + 8) + (OVERLAY ? 0 : (size_t)r * ring_pld(r));
     __shared__ int rq_flag;
     if (threadIdx.x == 0) rq_flag = 1 << 30;
-    S* rec = scal + 16;        // qp x (r+1): v of Q_k^{j1+s}, tau at [r]
-    S* Tsm = rec + (size_t)qp * (r + 1);  // T(p, s) at Tsm[p*TL + s]
-    S* wx = Tsm + (size_t)qp * TL;        // Y^* x, then T^* Y^* x
+    S* rec0 = scal + 16;       // qp x (r+1): v of Q_k^{j1+s}, tau at [r]
+    S* Tsm0 = rec0 + (size_t)qp * (r + 1);  // T(p, s) at Tsm[p*TL + s]
+    S* wx = Tsm0 + (size_t)qp * TL;       // Y^* x, then T^* Y^* x
     S* wy = wx + (qp + 8);
     S* zx = wy + (qp + 8);
     S* zy = zx + (qp + 8);
     S* wu = zy + (qp + 8);                // Y^* v (T column build)
-    S* strip = wu + (qp + 8);  // strip_cap rows x (r+1) (row-major)
+    S* ys1 = wu + (qp + 8);    // prefetch set (odd steps): y, B block, records, T
+    S* Cb1 = PF ? ys1 + XL : ys1;
+    S* rec1 = PF ? Cb1 + (size_t)r * (r + 1) : Cb1;
+    S* Tsm1 = PF ? rec1 + (size_t)qp * (r + 1) : rec1;
+    S* strip = PF ? Tsm1 + (size_t)qp * TL : ys1;  // strip_cap rows x (r+1) (row-major)
     const int LDC = r + 1;
     // sweep index by ticket (not blockIdx): a CTA only ever waits on a sweep whose CTA already
     // started, so a normal (non-cooperative) launch cannot deadlock when SMs are shared
@@ -636,7 +647,33 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
         pt[slot] += now_ - tc;                \
         tc = now_;                            \
     } while (0)
+    // cp.async of step kk's y column, catch-up records, T factor and B block into a buffer set
+    auto issue_step_loads = [&](int kk, S* ysb, S* Cbb, S* recb, S* Tsmb, int th0, int nth) {
+        const int me = tid - th0, mw = me >> 5, nw = nth >> 5;
+        if (me < 0 || me >= nth) return;
+        const int jbk = j + max(0, (kk - 1) * r + 1);
+        const int i1k = j + kk * r + 1, i2k = min(j + (kk + 1) * r, n);
+        const int b0k = j1 + kk * r + 1, mk = i2k - i1k + 1, nxk = i2k - b0k + 1;
+        const int Lk = (t > 0) ? min(j - 1 + (kk + 1) * r, n) - b0k + 1 : 0;
+        const int cBk = i1k + r - 1;
+        if (!(jbk <= n && nxk > 0)) return;
+        if (cBk <= n)
+            for (int i = me; i < nxk; i += nth) k1_ld(&ysb[i], &IDX(a.B, a.ldb, b0k + i, cBk));
+        if (t > 0 && Lk >= 1)
+            for (int s2 = mw; s2 < t; s2 += nw) {  // warp per record / per T column
+                const S* src = a.Qr + ((int64_t)s2 * K + kk) * (r + 1);
+                for (int c = lane; c <= r; c += 32) k1_ld(&recb[s2 * (r + 1) + c], src + c);
+                const S* tsrc = a.Tr + ((int64_t)s2 * K + kk) * a.TLD;
+                for (int p = lane; p <= s2; p += 32) k1_ld(&Tsmb[p * TL + s2], tsrc + p);
+            }
+        if (mk >= 2)
+            for (int cc = mw; cc < mk; cc += nw)
+                for (int ii = lane; ii < mk; ii += 32) k1_ld(&Cbb[ii + cc * LDC], &IDX(a.B, a.ldb, i1k + ii, i1k + cc));
+    };
+    bool pf_next = false;  // step k's loads were issued during step k-1
     for (int k = 0; k < kcount; ++k) {
+        const bool have = pf_next;
+        pf_next = false;
         if (t > 0) {
             if (tid == 0) {
                 const int need = min(k + 3, kprev);
@@ -660,6 +697,10 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
             __syncthreads();
         }
         K1_TICK(0);
+        S* const ys = (PF && (k & 1)) ? ys1 : ys0;
+        S* const Cb = (PF && (k & 1)) ? Cb1 : Cb0;
+        S* const rec = (PF && (k & 1)) ? rec1 : rec0;
+        S* const Tsm = (PF && (k & 1)) ? Tsm1 : Tsm0;
         const int jb = j + max(0, (k - 1) * r + 1);
         const int i1 = j + k * r + 1;
         const int i2 = min(j + (k + 1) * r, n);
@@ -680,22 +721,14 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
         const bool gen = (m >= 2) && jb <= n && nx > 0;
         const bool cu = (t > 0) && L >= 1 && jb <= n && nx > 0;  // catch-up present
         // ---- (S1) all loads of the step at once ------------------------------------------
+        // (y, records, T and the B block were prefetched during the previous step's RQ: they are
+        // final once sweep j-1 finished step k+2, which step k-1 already waited for)
         if (jb <= n && nx > 0) {
             if (k == 0)
                 for (int i = tid; i < nx; i += NT) k1_ld(&xcol[i], &IDX(a.A, a.lda, b0 + i, jb));
-            if (hasB)
-                for (int i = tid; i < nx; i += NT) k1_ld(&ys[i], &IDX(a.B, a.ldb, b0 + i, cB));
-            if (cu) {  // warp per record / per T column (no integer division in the loops)
-                for (int s2 = warp; s2 < t; s2 += NW) {
-                    const S* src = a.Qr + ((int64_t)s2 * K + k) * (r + 1);
-                    for (int c = lane; c <= r; c += 32) k1_ld(&rec[s2 * (r + 1) + c], src + c);
-                    const S* tsrc = a.Tr + ((int64_t)s2 * K + k) * a.TLD;
-                    for (int p = lane; p <= s2; p += 32) k1_ld(&Tsm[p * TL + s2], tsrc + p);
-                }
-            }
+            if (!have) issue_step_loads(k, ys, Cb, rec, Tsm, 0, NT);
             if (gen) {
                 for (int cc = warp; cc < m; cc += NW) {
-                    for (int ii = lane; ii < m; ii += 32) k1_ld(&Cb[ii + cc * LDC], &IDX(a.B, a.ldb, i1 + ii, i1 + cc));
                     for (int rr = lane; rr < stA; rr += 32) k1_ld(&strip[rr * SLD + cc], &IDX(a.A, a.lda, i4 + rr, i1 + cc));
                     for (int rr = lane; rr < stB; rr += 32)
                         k1_ld(&strip[(stA + rr) * SLD + cc], &IDX(a.B, a.ldb, i4 + rr, i1 + cc));
@@ -843,6 +876,14 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
                 }
                 K1_TICK(3);
                 // ---- (S5) RQ of the block -> Z_k^j ---------------------------------------------
+                if (PF && k + 1 < kcount) {  // next step's inputs land while the RQ runs (issued by
+                    // the warps the RQ does not use, if any)
+                    constexpr int RQT = rq_nthr<S, MAXM>();
+                    issue_step_loads(k + 1, (k & 1) ? ys0 : ys1, (k & 1) ? Cb0 : Cb1, (k & 1) ? rec0 : rec1,
+                                     (k & 1) ? Tsm0 : Tsm1, RQT < NT ? RQT : 0, RQT < NT ? NT - RQT : NT);
+                    asm volatile("cp.async.commit_group;\n" ::: "memory");
+                    pf_next = true;
+                }
                 if (tid < rq_nthr<S, MAXM>()) rq_dir<S, MAXM>(m, Cb, LDC, ring, &rq_flag, uu);
                 __syncthreads();
                 if (tid == 0) rq_flag = 1 << 30;
