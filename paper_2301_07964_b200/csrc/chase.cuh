@@ -741,49 +741,44 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
         if (jb <= n && nx > 0) {
             // ---- (S2) catch-up in WY form: x(0:L) <- x - Y T^* Y^* x (same for y) ----------------
             if (cu) {
-                // round 1: w_s = Y(:,s)^* x, s < t (thread per (vector, s))
-                for (int e = tid; e < 2 * t; e += NT) {
-                    const int s = e % t;
-                    const bool isy = e >= t;
-                    if (isy && !hasB) continue;
-                    const S* v = rec + (size_t)s * (r + 1);
-                    const S* xv = isy ? ys : xcol;
-                    const int ms = min(r, n - (j1 + s + k * r));
-                    S d0 = S(0.0), d1 = S(0.0);
-                    int i = 0;
-                    for (; i + 1 < ms; i += 2) {
-                        d0 += conj_mul(v[i], xv[s + i]);
-                        d1 += conj_mul(v[i + 1], xv[s + i + 1]);
+                // warp 0 catches x up, warp 1 catches y up: three warp-synchronous rounds each
+                if (warp < 2 && (warp == 0 || hasB)) {
+                    const bool isy = warp == 1;
+                    S* xv = isy ? ys : xcol;
+                    S* wv = isy ? wy : wx;
+                    S* zv = isy ? zy : zx;
+                    // round 1: w_s = Y(:,s)^* x, s < t
+                    for (int s2 = lane; s2 < t; s2 += 32) {
+                        const S* v = rec + (size_t)s2 * (r + 1);
+                        const int ms = min(r, n - (j1 + s2 + k * r));
+                        S d0 = S(0.0), d1 = S(0.0);
+                        int i = 0;
+                        for (; i + 1 < ms; i += 2) {
+                            d0 += conj_mul(v[i], xv[s2 + i]);
+                            d1 += conj_mul(v[i + 1], xv[s2 + i + 1]);
+                        }
+                        if (i < ms) d0 += conj_mul(v[i], xv[s2 + i]);
+                        if (is_zero(v[r])) d0 = d1 = S(0.0);  // tau = 0: Q = I (record may be empty)
+                        wv[s2] = d0 + d1;
                     }
-                    if (i < ms) d0 += conj_mul(v[i], xv[s + i]);
-                    if (is_zero(v[r])) d0 = d1 = S(0.0);  // tau = 0: Q = I (record may be empty)
-                    (isy ? wy : wx)[s] = d0 + d1;
-                }
-                __syncthreads();
-                // round 2: z = T^* w  (z_s = sum_{p<=s} conj(T(p,s)) w_p)
-                for (int e = tid; e < 2 * t; e += NT) {
-                    const int s = e % t;
-                    const bool isy = e >= t;
-                    if (isy && !hasB) continue;
-                    const S* wv = isy ? wy : wx;
-                    S z = S(0.0);
-                    for (int p = 0; p <= s; ++p) z += conj_mul(Tsm[p * TL + s], wv[p]);
-                    (isy ? zy : zx)[s] = z;
-                }
-                __syncthreads();
-                // round 3: x(i) -= sum_s Y(i,s) z_s over reflectors covering row i
-                for (int e = tid; e < 2 * L; e += NT) {
-                    const int i = e % L;
-                    const bool isy = e >= L;
-                    if (isy && !hasB) continue;
-                    const S* z = isy ? zy : zx;
-                    S acc = S(0.0);
-                    const int slo = max(0, i - r + 1), shi = min(t - 1, i);
-                    for (int s = slo; s <= shi; ++s) {
-                        const int ms = min(r, n - (j1 + s + k * r));
-                        if (i - s < ms) acc += rec[(size_t)s * (r + 1) + (i - s)] * z[s];
+                    __syncwarp();
+                    // round 2: z = T^* w  (z_s = sum_{p<=s} conj(T(p,s)) w_p)
+                    for (int s2 = lane; s2 < t; s2 += 32) {
+                        S z = S(0.0);
+                        for (int p = 0; p <= s2; ++p) z += conj_mul(Tsm[p * TL + s2], wv[p]);
+                        zv[s2] = z;
                     }
-                    (isy ? ys : xcol)[i] -= acc;
+                    __syncwarp();
+                    // round 3: x(i) -= sum_s Y(i,s) z_s over reflectors covering row i
+                    for (int i = lane; i < L; i += 32) {
+                        S acc = S(0.0);
+                        const int slo = max(0, i - r + 1), shi = min(t - 1, i);
+                        for (int s2 = slo; s2 <= shi; ++s2) {
+                            const int ms = min(r, n - (j1 + s2 + k * r));
+                            if (i - s2 < ms) acc += rec[(size_t)s2 * (r + 1) + (i - s2)] * zv[s2];
+                        }
+                        xv[i] -= acc;
+                    }
                 }
                 __syncthreads();
                 if (hasB && gen) {
@@ -836,11 +831,26 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
                 if (warp < NW / 2) {
                     if (!is_zero(tau)) {
                         const S ctau = conjv(tau);
-                        for (int c = warp; c < m; c += NW / 2) {
-                            S s = S(0.0);
-                            for (int i = lane; i < m; i += 32) s += conj_mul(vq[i], Cb[i + c * LDC]);
-                            s = warp_sum(s) * ctau;
-                            for (int i = lane; i < m; i += 32) Cb[i + c * LDC] -= vq[i] * s;
+                        if (m <= 32) {  // warp 0: lane per column, no reductions
+                            if (warp == 0 && lane < m) {
+                                S* col = Cb + lane * LDC;
+                                S s0 = S(0.0), s1 = S(0.0);
+                                int i = 0;
+                                for (; i + 1 < m; i += 2) {
+                                    s0 += conj_mul(vq[i], col[i]);
+                                    s1 += conj_mul(vq[i + 1], col[i + 1]);
+                                }
+                                if (i < m) s0 += conj_mul(vq[i], col[i]);
+                                const S sc = (s0 + s1) * ctau;
+                                for (i = 0; i < m; ++i) col[i] -= vq[i] * sc;
+                            }
+                        } else {
+                            for (int c = warp; c < m; c += NW / 2) {
+                                S s = S(0.0);
+                                for (int i = lane; i < m; i += 32) s += conj_mul(vq[i], Cb[i + c * LDC]);
+                                s = warp_sum(s) * ctau;
+                                for (int i = lane; i < m; i += 32) Cb[i + c * LDC] -= vq[i] * s;
+                            }
                         }
                     }
                 } else {
