@@ -34,6 +34,9 @@ struct ChaseArgs {
     S* Zr;      // (qp*K) records of (r+1): v of Z_k^j, sigma at [r]
     S* Tr;      // (qp*K) records of TLD: column t of window k's WY factor T (rows 0..t)
     int TLD;
+    S* Mg;        // K blocks of mst: M_t(k) = (Q_k^{j1+t-1})^* ... (Q_k^{j1})^*, the catch-up operator
+    int mld;      // of sweep t on window k (row-major, ld mld), updated in place sweep by sweep
+    int64_t mst;  // (dense path only: chase_dense_catchup)
     int* prog;  // prog[0..qp): steps completed by each sweep; prog[qp]: ticket;
                 // prog[qp+1 .. 2qp+1): far-strip items completed by each helper
     int strip_cap;  // strip rows (A then B) staged in shared memory per step
@@ -472,6 +475,14 @@ __device__ __forceinline__ void rq_dir(int m, const S* Cb, int LDC, S* ring, vol
 // >= r + 4 also covers the unrolled variant's MAXM + 4)
 __host__ __device__ inline int ring_pld(int r) { return r <= 32 ? r + 20 : (r <= 64 ? 68 : 132); }
 
+// Dense catch-up operator (real r <= 32, complex r <= 16: the unrolled RQ leaves 6 warps idle):
+// sweep t keeps M_t(k) (L x L) instead of records + WY factor; the idle warps form
+// M_{t+1}(k) = (Q_k^j)^* M_t(k) during the RQ and store it for sweep t+1.
+template <typename S>
+__host__ __device__ constexpr bool chase_dense_catchup(int r) {
+    return r <= 64 && r * (int)sizeof(S) <= 256;
+}
+
 template <typename S>
 __host__ __device__ inline size_t chase_smem_elems(int r, int qp, int strip_cap) {
     const int w = qp + r - 1;
@@ -486,6 +497,7 @@ __host__ __device__ inline size_t chase_smem_elems(int r, int qp, int strip_cap)
            (size_t)qp * (qp + 1) +       // T factor of window k
            5 * (size_t)(qp + 8) +        // WY temporaries
            (overlay ? 0 : XL + (size_t)r * (r + 1) + (size_t)qp * (r + 1) + (size_t)qp * (qp + 1)) +  // prefetch set
+           (chase_dense_catchup<S>(r) ? 2 * (size_t)w * (w | 1) + 2 * (size_t)(w + 1) : 0) +  // M_t, M_t(k+1), tmp
            (size_t)strip_cap * (r + 1);  // staged strip rows
 }
 
@@ -620,7 +632,13 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
     S* Cb1 = PF ? ys1 + XL : ys1;
     S* rec1 = PF ? Cb1 + (size_t)r * (r + 1) : Cb1;
     S* Tsm1 = PF ? rec1 + (size_t)qp * (r + 1) : rec1;
-    S* strip = PF ? Tsm1 + (size_t)qp * TL : ys1;  // strip_cap rows x (r+1) (row-major)
+    // (MAXM is the smallest of 8/16/32/64/128 >= r, so this is chase_dense_catchup<S>(r))
+    constexpr bool MK = PF && rq_nthr<S, MAXM>() < NT && chase_dense_catchup<S>(MAXM);
+    const int MLD = a.mld;
+    S* Msm0 = PF ? Tsm1 + (size_t)qp * TL : ys1;  // M_t(k), even / odd steps (L x L, ld MLD)
+    S* Msm1 = MK ? Msm0 + (size_t)w * MLD : Msm0;
+    S* mtmp = MK ? Msm1 + (size_t)w * MLD : Msm0;  // 2 (w+1): catch-up outputs / M update row
+    S* strip = MK ? mtmp + 2 * (size_t)(w + 1) : Msm0;  // strip_cap rows x (r+1) (row-major)
     const int LDC = r + 1;
     // sweep index by ticket (not blockIdx): a CTA only ever waits on a sweep whose CTA already
     // started, so a normal (non-cooperative) launch cannot deadlock when SMs are shared
@@ -648,7 +666,7 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
         tc = now_;                            \
     } while (0)
     // cp.async of step kk's y column, catch-up records, T factor and B block into a buffer set
-    auto issue_step_loads = [&](int kk, S* ysb, S* Cbb, S* recb, S* Tsmb, int th0, int nth) {
+    auto issue_step_loads = [&](int kk, S* ysb, S* Cbb, S* recb, S* Tsmb, S* Mb, int th0, int nth) {
         const int me = tid - th0, mw = me >> 5, nw = nth >> 5;
         if (me < 0 || me >= nth) return;
         const int jbk = j + max(0, (kk - 1) * r + 1);
@@ -659,7 +677,12 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
         if (!(jbk <= n && nxk > 0)) return;
         if (cBk <= n)
             for (int i = me; i < nxk; i += nth) k1_ld(&ysb[i], &IDX(a.B, a.ldb, b0k + i, cBk));
-        if (t > 0 && Lk >= 1)
+        if (MK && t > 0 && Lk >= 1) {
+            const S* src = a.Mg + (int64_t)kk * a.mst;
+            for (int i = mw; i < Lk; i += nw)
+                for (int c = lane; c < Lk; c += 32) k1_ld(&Mb[i * MLD + c], src + (size_t)i * MLD + c);
+        }
+        if (!MK && t > 0 && Lk >= 1)
             for (int s2 = mw; s2 < t; s2 += nw) {  // warp per record / per T column
                 const S* src = a.Qr + ((int64_t)s2 * K + kk) * (r + 1);
                 for (int c = lane; c <= r; c += 32) k1_ld(&recb[s2 * (r + 1) + c], src + c);
@@ -701,6 +724,7 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
         S* const Cb = (PF && (k & 1)) ? Cb1 : Cb0;
         S* const rec = (PF && (k & 1)) ? rec1 : rec0;
         S* const Tsm = (PF && (k & 1)) ? Tsm1 : Tsm0;
+        S* const Msm = (PF && (k & 1)) ? Msm1 : Msm0;
         const int jb = j + max(0, (k - 1) * r + 1);
         const int i1 = j + k * r + 1;
         const int i2 = min(j + (k + 1) * r, n);
@@ -726,7 +750,7 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
         if (jb <= n && nx > 0) {
             if (k == 0)
                 for (int i = tid; i < nx; i += NT) k1_ld(&xcol[i], &IDX(a.A, a.lda, b0 + i, jb));
-            if (!have) issue_step_loads(k, ys, Cb, rec, Tsm, 0, NT);
+            if (!have) issue_step_loads(k, ys, Cb, rec, Tsm, Msm, 0, NT);
             if (gen) {
                 for (int cc = warp; cc < m; cc += NW) {
                     for (int rr = lane; rr < stA; rr += 32) k1_ld(&strip[rr * SLD + cc], &IDX(a.A, a.lda, i4 + rr, i1 + cc));
@@ -741,8 +765,31 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
         if (jb <= n && nx > 0) {
             // ---- (S2) catch-up in WY form: x(0:L) <- x - Y T^* Y^* x (same for y) ----------------
             if (cu) {
-                // warp 0 catches x up, warp 1 catches y up: three warp-synchronous rounds each
-                if (warp < 2 && (warp == 0 || hasB)) {
+                if constexpr (MK) {  // x <- M_t x, y <- M_t y (one round, thread per output row)
+                    for (int e = tid; e < 2 * L; e += NT) {
+                        const bool isy = e >= L;
+                        if (isy && !hasB) continue;
+                        const S* xv = isy ? ys : xcol;
+                        const S* mr = Msm + (size_t)(isy ? e - L : e) * MLD;
+                        S a0 = S(0.0), a1 = S(0.0), a2 = S(0.0), a3 = S(0.0);
+                        int c = 0;
+                        for (; c + 3 < L; c += 4) {
+                            a0 = fma_s(mr[c], xv[c], a0);
+                            a1 = fma_s(mr[c + 1], xv[c + 1], a1);
+                            a2 = fma_s(mr[c + 2], xv[c + 2], a2);
+                            a3 = fma_s(mr[c + 3], xv[c + 3], a3);
+                        }
+                        for (; c < L; ++c) a0 = fma_s(mr[c], xv[c], a0);
+                        mtmp[e] = (a0 + a1) + (a2 + a3);
+                    }
+                    __syncthreads();
+                    for (int e = tid; e < 2 * L; e += NT) {
+                        const bool isy = e >= L;
+                        if (isy && !hasB) continue;
+                        (isy ? ys : xcol)[isy ? e - L : e] = mtmp[e];
+                    }
+                } else if (warp < 2 && (warp == 0 || hasB)) {
+                    // warp 0 catches x up, warp 1 catches y up: three warp-synchronous rounds each
                     const bool isy = warp == 1;
                     S* xv = isy ? ys : xcol;
                     S* wv = isy ? wy : wx;
@@ -797,6 +844,14 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
                 for (int i = tid; i < L; i += NT) IDX(a.A, a.lda, b0 + i, jb) = xcol[i];
                 if (hasB)
                     for (int i = tid; i < L; i += NT) IDX(a.B, a.ldb, b0 + i, cB) = ys[i];
+                if (MK && t + 1 < qp) {  // M_{t+1}(k) = M_t(k) (Q = I), extended by identity
+                    const int Ln = min(j + (k + 1) * r, n) - b0 + 1;
+                    const int Lc = cu ? L : 0;
+                    S* dst = a.Mg + (int64_t)k * a.mst;
+                    for (int i = warp; i < Ln; i += NW)
+                        for (int c = lane; c < Ln; c += 32)
+                            dst[(size_t)i * MLD + c] = (i < Lc && c < Lc) ? Msm[i * MLD + c] : S(i == c ? 1.0 : 0.0);
+                }
             } else {
                 __syncthreads();
                 K1_TICK(2);
@@ -853,7 +908,7 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
                             }
                         }
                     }
-                } else {
+                } else if (!MK) {
                     // xLARFT column t: T(0:t,t) = -tau T(0:t,0:t) (Y(:,0:t)^* v), T(t,t) = tau
                     const int hn = NT - NT / 2, me = tid - NT / 2;
                     for (int s = me; s < t; s += hn) {
@@ -890,9 +945,43 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
                     // the warps the RQ does not use, if any)
                     constexpr int RQT = rq_nthr<S, MAXM>();
                     issue_step_loads(k + 1, (k & 1) ? ys0 : ys1, (k & 1) ? Cb0 : Cb1, (k & 1) ? rec0 : rec1,
-                                     (k & 1) ? Tsm0 : Tsm1, RQT < NT ? RQT : 0, RQT < NT ? NT - RQT : NT);
+                                     (k & 1) ? Tsm0 : Tsm1, (k & 1) ? Msm0 : Msm1, RQT < NT ? RQT : 0, RQT < NT ? NT - RQT : NT);
                     asm volatile("cp.async.commit_group;\n" ::: "memory");
                     pf_next = true;
+                }
+                if constexpr (MK) {
+                    // the idle warps form M_{t+1}(k) = (Q_k^j)^* M_t(k) for sweep t+1 (in place in Mg)
+                    constexpr int RQT = rq_nthr<S, MAXM>();
+                    if (t + 1 < qp && tid >= RQT) {
+                        const int nth = NT - RQT, me = tid - RQT, mw = me >> 5, nw = nth >> 5;
+                        const int Ln = min(j + (k + 1) * r, n) - b0 + 1;
+                        const int Lc = cu ? L : 0;  // M_0 = I
+                        auto base = [&](int i, int c) -> S {
+                            return (i < Lc && c < Lc) ? Msm[i * MLD + c] : S(i == c ? 1.0 : 0.0);
+                        };
+                        const S ctau = conjv(tau);
+                        for (int c = me; c < Ln; c += nth) {  // d_c = conj(tau) v^* M(t:t+m, c)
+                            S d0 = S(0.0), d1 = S(0.0);
+                            int p2 = 0;
+                            for (; p2 + 1 < m; p2 += 2) {
+                                d0 += conj_mul(vq[p2], base(t + p2, c));
+                                d1 += conj_mul(vq[p2 + 1], base(t + p2 + 1, c));
+                            }
+                            if (p2 < m) d0 += conj_mul(vq[p2], base(t + p2, c));
+                            mtmp[c] = (d0 + d1) * ctau;
+                        }
+                        named_bar(3, nth);
+                        S* dst = a.Mg + (int64_t)k * a.mst;
+                        for (int i = mw; i < Ln; i += nw) {
+                            const bool upd = i >= t && i < t + m;
+                            const S vi = upd ? vq[i - t] : S(0.0);
+                            for (int c = lane; c < Ln; c += 32) {
+                                S val = base(i, c);
+                                if (upd) val -= vi * mtmp[c];
+                                dst[(size_t)i * MLD + c] = val;
+                            }
+                        }
+                    }
                 }
                 if (tid < rq_nthr<S, MAXM>()) rq_dir<S, MAXM>(m, Cb, LDC, ring, &rq_flag, uu);
                 __syncthreads();
@@ -988,6 +1077,7 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
             st_release(&a.prog[t], k + 1);
         }
         cur ^= 1;
+        pt[11] += 1;  // step count (not a time slot)
     }
     if (a.prof && tid == 0 && (a.prof_t0 < 0 || t == a.prof_t0))
         for (int i = 0; i < 12; ++i) atomicAdd((unsigned long long*)&a.prof[i], (unsigned long long)pt[i]);

@@ -180,9 +180,13 @@ struct Plan {
 // stream while later groups are chased; the side stream may lag NUV-1 groups), reflector
 // records, WY factors, progress counters.
 constexpr int NUV = 4;
+// dense catch-up operators M_t(k) (chase_dense_catchup): one (q+r-1) x ((q+r-1)|1) block per window
+inline int mcatch_ld(int q, int r) { return (q + r - 1) | 1; }
+inline int64_t mcatch_st(int q, int r) { return (int64_t)(q + r - 1) * mcatch_ld(q, r); }
+
 template <typename S>
 struct Workspace {
-    S *U[NUV] = {}, *V[NUV] = {}, *MU[NUV] = {}, *MV[NUV] = {}, *Zr = nullptr, *Qr = nullptr, *Tr = nullptr;
+    S *U[NUV] = {}, *V[NUV] = {}, *MU[NUV] = {}, *MV[NUV] = {}, *Zr = nullptr, *Qr = nullptr, *Tr = nullptr, *Mg = nullptr;
     int* prog = nullptr;
     long long* k1prof = nullptr;
     long long k1prof_host[12] = {0};
@@ -210,6 +214,7 @@ struct Workspace {
         CK(mal((void**)&Zr, rec));
         CK(mal((void**)&Qr, rec));
         CK(mal((void**)&Tr, tf));
+        if (chase_dense_catchup<S>(p.r)) CK(mal((void**)&Mg, (size_t)p.Kmax * mcatch_st(p.q, p.r) * sizeof(S)));
         CK(mal((void**)&prog, (size_t)(5 * p.q + 2) * sizeof(int)));
         if (k1p) {
             CK(mal((void**)&k1prof, 12 * sizeof(long long)));
@@ -244,6 +249,8 @@ struct Workspace {
         CK(fr(Zr));
         CK(fr(Qr));
         CK(fr(Tr));
+        if (Mg) CK(fr(Mg));
+        Mg = nullptr;
         CK(fr(prog));
         CK(fr(k1prof));
         for (int b = 0; b < NUV; ++b) {
@@ -256,12 +263,15 @@ struct Workspace {
 };
 
 void print_k1prof(const long long* h) {
-    const char* nm[12] = {"wait", "loads", "catchup", "QB+T", "larfgZ", "strip", "RQ", "larfgQ", "writes", "waitH", "s10", "s11"};
+    const char* nm[11] = {"wait", "loads", "catchup", "QB+T", "larfgZ", "strip", "RQ", "larfgQ", "writes", "waitH", "s10"};
     double tot = 0;
-    for (int i = 0; i < 12; ++i) tot += (double)h[i];
+    for (int i = 0; i < 11; ++i) tot += (double)h[i];
+    const double steps = h[11] > 0 ? (double)h[11] : 1.0;  // slot 11 counts steps
     fprintf(stderr, "K1 cycles (sum over CTAs):");
-    for (int i = 0; i < 12; ++i) fprintf(stderr, " %s=%.1f%%", nm[i], 100.0 * h[i] / (tot > 0 ? tot : 1));
-    fprintf(stderr, " total=%.3g\n", tot);
+    for (int i = 0; i < 11; ++i) fprintf(stderr, " %s=%.1f%%", nm[i], 100.0 * h[i] / (tot > 0 ? tot : 1));
+    fprintf(stderr, " total=%.3g steps=%.0f\nK1 cycles per step:", tot, steps);
+    for (int i = 0; i < 11; ++i) fprintf(stderr, " %s=%.0f", nm[i], h[i] / steps);
+    fprintf(stderr, " all=%.0f\n", tot / steps);
 }
 
 // Enqueue every group of the reduction: chase (K1) -> accumulate U/V (K2) -> H/T right and left
@@ -342,7 +352,8 @@ int enqueue_groups(const Plan<S>& p, Workspace<S>& ws, cudaStream_t stream, bool
             CK(cudaMemsetAsync(ws.prog, 0, (size_t)((1 + p.helpers) * q + 1) * sizeof(int), stream));
             CK(cudaMemsetAsync(ws.Qr, 0, (size_t)qp * K * (r + 1) * sizeof(S), stream));
             CK(cudaMemsetAsync(ws.Zr, 0, (size_t)qp * K * (r + 1) * sizeof(S), stream));
-            ChaseArgs<S> ca{n, r, qp, j1, K, p.H, p.ldh, p.T, p.ldt, ws.Qr, ws.Zr, ws.Tr, TLD, ws.prog, p.strip_cap,
+            ChaseArgs<S> ca{n, r, qp, j1, K, p.H, p.ldh, p.T, p.ldt, ws.Qr, ws.Zr, ws.Tr, TLD, ws.Mg,
+                            mcatch_ld(q, r), mcatch_st(q, r), ws.prog, p.strip_cap,
                             p.helpers, ws.k1prof, getenv("HT_K1PROF_T") ? atoi(getenv("HT_K1PROF_T")) : -1};
             void* kargs[] = {&ca};
             CK(cudaLaunchKernel(p.chase_fn, dim3(qp * (1 + p.helpers)), dim3(CHASE_NT), kargs, p.chase_bytes, stream));
