@@ -69,6 +69,9 @@ __device__ __forceinline__ void k1_ld(S* s, const S* g) { k1_cp_async(s, g, (int
 __device__ __forceinline__ void k1_commit_wait() {
     asm volatile("cp.async.commit_group;\ncp.async.wait_all;\n" ::: "memory");
 }
+__device__ __forceinline__ void k1_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void k1_wait_group() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 // Stage flag of the RQ's two warp groups.  The producer publishes after a named barrier that
 // orders every producer thread's ring writes before the flag store; shared-memory stores of one
 // SM are performed in issue order, so a volatile store suffices (no MEMBAR on the RQ chain).
@@ -751,6 +754,10 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
             if (k == 0)
                 for (int i = tid; i < nx; i += NT) k1_ld(&xcol[i], &IDX(a.A, a.lda, b0 + i, jb));
             if (!have) issue_step_loads(k, ys, Cb, rec, Tsm, Msm, 0, NT);
+        }
+        k1_commit();
+        // the strip is only needed after the RQ: its own (newest) group, waited for there
+        if (jb <= n && nx > 0) {
             if (gen) {
                 for (int cc = warp; cc < m; cc += NW) {
                     for (int rr = lane; rr < stA; rr += 32) k1_ld(&strip[rr * SLD + cc], &IDX(a.A, a.lda, i4 + rr, i1 + cc));
@@ -759,7 +766,9 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
                 }
             }
         }
-        k1_commit_wait();
+        k1_commit();
+        K1_TICK(10);
+        k1_wait_group<1>();
         __syncthreads();
         K1_TICK(1);
         if (jb <= n && nx > 0) {
@@ -828,15 +837,9 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
                     }
                 }
                 __syncthreads();
-                if (hasB && gen) {
+                if (hasB && gen)
                     for (int i = tid; i < m; i += NT)
                         if (t + i < L) Cb[i + (m - 1) * LDC] = ys[t + i];
-                    // caught-up rows b0..i1-1 of column i2 are also rows of the staged B strip
-                    for (int i = tid; i < t && i < L; i += NT) {
-                        const int rr = (b0 + i) - i4;
-                        if (rr >= 0 && rr < stB) strip[(stA + rr) * SLD + (m - 1)] = ys[i];
-                    }
-                }
             }
             if (hasB && gen && !cu)
                 for (int i = tid; i < m; i += NT) Cb[i + (m - 1) * LDC] = ys[t + i];
@@ -880,10 +883,26 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
                     for (int c = tid; c < m; c += NT) qr[c] = vq[c];
                     if (tid == 0) qr[r] = tau;
                 }
-                __syncthreads();
+                if constexpr (!MK) __syncthreads();  // (the dense path's Q^*B reads none of it)
                 K1_TICK(8);
                 // ---- (S4) B block <- Q^* B block (warps 0..NW/2-1) || T column t (others) ------
-                if (warp < NW / 2) {
+                if constexpr (MK) {
+                    // m <= 32: a group of G lanes per column, one element per lane
+                    if (!is_zero(tau)) {
+                        const S ctau = conjv(tau);
+                        const int G = m <= 8 ? 8 : (m <= 16 ? 16 : 32), CPW = 32 / G;
+                        const int i = lane & (G - 1);
+                        const S vi = i < m ? vq[i] : S(0.0);
+                        for (int base = warp * CPW; base < m; base += NW * CPW) {
+                            const int c = base + lane / G;
+                            const bool ok = c < m && i < m;
+                            const S e = ok ? Cb[i + c * LDC] : S(0.0);
+                            S d = conj_mul(vi, e);
+                            for (int o = 1; o < G; o <<= 1) d += shfl_xor(d, o);
+                            if (ok) Cb[i + c * LDC] = e - vi * (d * ctau);
+                        }
+                    }
+                } else if (warp < NW / 2) {
                     if (!is_zero(tau)) {
                         const S ctau = conjv(tau);
                         if (m <= 32) {  // warp 0: lane per column, no reductions
@@ -984,6 +1003,8 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
                     }
                 }
                 if (tid < rq_nthr<S, MAXM>()) rq_dir<S, MAXM>(m, Cb, LDC, ring, &rq_flag, uu);
+                if (pf_next) k1_wait_group<1>();  // the strip (the prefetch group may stay in flight)
+                else k1_wait_group<0>();
                 __syncthreads();
                 if (tid == 0) rq_flag = 1 << 30;
                 K1_TICK(6);
@@ -992,6 +1013,12 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
                     double b2;
                     warp_larfg(m, uu, vz, sig, b2);
                     if (lane == 0) scal[2] = sig;
+                } else if (hasB && cu) {
+                    // caught-up rows b0..i1-1 of column i2 are also rows of the staged B strip
+                    for (int i = tid - 32; i < t && i < L; i += NT - 32) {
+                        const int rr = (b0 + i) - i4;
+                        if (rr >= 0 && rr < stB) strip[(stA + rr) * SLD + (m - 1)] = ys[i];
+                    }
                 }
                 __syncthreads();
                 K1_TICK(4);
@@ -1072,7 +1099,7 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
             for (int i = tid; i < nxn; i += NT) xnext[i] = ldcg(&IDX(a.A, a.lda, bn + i, jbn));
             __syncthreads();
         }
-        if (tid == 0) {
+        if (tid == NT - 32) {  // (not thread 0: it spins on the previous sweep meanwhile)
             __threadfence();
             st_release(&a.prog[t], k + 1);
         }
