@@ -114,6 +114,32 @@ __device__ __forceinline__ void warp_larfg(int m, const S* x, S* vout, S& tau, d
     __syncwarp();
 }
 
+// Register form of the same reflector for m <= 32 (lane l holds x[l]; lanes >= m hold 0), with
+// the MUFU-seeded rsqrt / reciprocal of the RQ instead of IEEE sqrt and division:
+// beta = -sign(re alpha) ||x||, tau = 1 - alpha / beta (beta real), v = x / (alpha - beta).
+// Returns v[lane] (v[0] = 1).
+__device__ __forceinline__ double fast_recip_s(double d) { return fast_rcp(d); }
+__device__ __forceinline__ zc fast_recip_s(zc d) { return conjv(d) * fast_rcp(abs2(d)); }
+template <typename S>
+__device__ __forceinline__ S larfg_reg(S xv, int m, S& tau, double& beta) {
+    const int lane = threadIdx.x & 31;
+    const S alpha = shfl_idx(xv, 0);
+    double s = (lane >= 1 && lane < m) ? abs2(xv) : 0.0;
+    s = warp_sum(s);
+    if (s == 0.0 && im(alpha) == 0.0) {
+        tau = S(0.0);
+        beta = re(alpha);
+        return S(lane == 0 ? 1.0 : 0.0);
+    }
+    const double a2 = abs2(alpha) + s;
+    const double rs = fast_rsqrt(a2);
+    const bool pos = re(alpha) >= 0.0;
+    beta = pos ? -(a2 * rs) : a2 * rs;
+    tau = S(1.0) - alpha * (pos ? -rs : rs);
+    const S sc = fast_recip_s(alpha - S(beta));
+    return lane == 0 ? S(1.0) : xv * sc;
+}
+
 // RQ thread layout.  Group A (threads [0, NA)) holds the m rows of C, group B (threads
 // [NA, 2NA)) the m rows of P; LPR threads per row, each with E columns in REGISTERS, columns
 // interleaved (thread part p holds columns LPR*e + p) so that the per-stage skip of the columns
@@ -610,7 +636,8 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
     constexpr int NW = NT / 32;
     const int XL = w + r + 8;
     const int TL = qp + 1;
-    S* xc[2] = {sm, sm + XL};  // column jb of this step / of the next step
+    // column jb of this step / of the next step: sm + cur * XL (pointer arithmetic on the shared
+    // base, not a pointer table, so accesses stay LDS/STS instead of generic loads)
     S* ys0 = sm + 2 * XL;
     constexpr bool OVERLAY = MAXM > 64;  // RQ ring overlays Cb (the block goes to HBM after Q^*)
     constexpr bool PF = !OVERLAY;        // next step's B block / records / T / y prefetched during the RQ
@@ -660,10 +687,12 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
     const int kcount = min(K, 2 + (n - j - 1) / r);
     const int kprev = (t > 0) ? min(K, 2 + (n - j) / r) : 0;
     int cur = 0;
-    long long pt[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+    long long pt[16] = {};
     long long tc = clock64();
+    // (the shared load makes a preceding barrier's deferred block land before the clock read)
 #define K1_TICK(slot)                         \
     do {                                      \
+        if (a.prof) (void)*(volatile int*)&t_sh; \
         const long long now_ = clock64();     \
         pt[slot] += now_ - tc;                \
         tc = now_;                            \
@@ -741,8 +770,8 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
         const int nx = i2 - b0 + 1;
         const int cB = i1 + r - 1;  // == i2 when it exists
         const bool hasB = cB <= n;
-        S* xcol = xc[cur];
-        S* xnext = xc[cur ^ 1];
+        S* xcol = sm + (cur ? XL : 0);
+        S* xnext = sm + (cur ? 0 : XL);
         const int nA = max(0, i3 - i4 + 1), nBs = max(0, i1 - i4);  // strip rows (B: above block)
         const int stA = min(nA, a.strip_cap), stB = min(nBs, a.strip_cap - stA);
         const bool gen = (m >= 2) && jb <= n && nx > 0;
@@ -756,6 +785,7 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
             if (!have) issue_step_loads(k, ys, Cb, rec, Tsm, Msm, 0, NT);
         }
         k1_commit();
+        K1_TICK(1);
         // the strip is only needed after the RQ: its own (newest) group, waited for there
         if (jb <= n && nx > 0) {
             if (gen) {
@@ -773,7 +803,8 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
         K1_TICK(1);
         if (jb <= n && nx > 0) {
             // ---- (S2) catch-up in WY form: x(0:L) <- x - Y T^* Y^* x (same for y) ----------------
-            if (cu) {
+            // (dense path with a reflector: merged with S3 below)
+            if (cu && !(MK && gen)) {
                 if constexpr (MK) {  // x <- M_t x, y <- M_t y (one round, thread per output row)
                     for (int e = tid; e < 2 * L; e += NT) {
                         const bool isy = e >= L;
@@ -841,7 +872,7 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
                     for (int i = tid; i < m; i += NT)
                         if (t + i < L) Cb[i + (m - 1) * LDC] = ys[t + i];
             }
-            if (hasB && gen && !cu)
+            if (!MK && hasB && gen && !cu)
                 for (int i = tid; i < m; i += NT) Cb[i + (m - 1) * LDC] = ys[t + i];
             if (!gen) {  // catch-up only (no reflector at this step; Alg. 2 has m >= 2)
                 for (int i = tid; i < L; i += NT) IDX(a.A, a.lda, b0 + i, jb) = xcol[i];
@@ -856,21 +887,72 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
                             dst[(size_t)i * MLD + c] = (i < Lc && c < Lc) ? Msm[i * MLD + c] : S(i == c ? 1.0 : 0.0);
                 }
             } else {
+                S tau;
+                if constexpr (MK) {
+                    // ---- (S2+S3) dense catch-up fused with the left reflector ------------------
+                    // warp 0: caught-up rows t..t+m-1 of x, one per lane, straight into the reflector;
+                    // warps 1..: rows 0..t-1 of x and rows 0..L-1 of y into mtmp ([0,t) / [L,2L)),
+                    // y rows t..t+m-1 also into the B block's last column
+                    auto mdot = [&](int row, const S* v) -> S {
+                        const S* mr = Msm + (size_t)row * MLD;
+                        S a0 = S(0.0), a1 = S(0.0), a2 = S(0.0), a3 = S(0.0);
+                        int c = 0;
+                        for (; c + 3 < L; c += 4) {
+                            a0 = fma_s(mr[c], v[c], a0);
+                            a1 = fma_s(mr[c + 1], v[c + 1], a1);
+                            a2 = fma_s(mr[c + 2], v[c + 2], a2);
+                            a3 = fma_s(mr[c + 3], v[c + 3], a3);
+                        }
+                        for (; c < L; ++c) a0 = fma_s(mr[c], v[c], a0);
+                        return (a0 + a1) + (a2 + a3);
+                    };
+                    if (warp == 0) {
+                        const int row = t + lane;
+                        S xv = S(0.0);
+                        if (lane < m) xv = (row < L) ? mdot(row, xcol) : xcol[row];
+                        S tq;
+                        double beta;
+                        const S vl = larfg_reg(xv, m, tq, beta);
+                        if (lane < m) vq[lane] = vl;
+                        if (lane == 0) {
+                            scal[0] = tq;
+                            scal[1] = S(beta);
+                        }
+                    } else {
+                        const int ny = hasB ? L : 0;
+                        for (int e = tid - 32; e < t + ny; e += NT - 32) {
+                            if (e < t) {
+                                mtmp[e] = mdot(e, xcol);
+                            } else {
+                                const int i = e - t;
+                                const S val = mdot(i, ys);
+                                mtmp[L + i] = val;
+                                if (gen && i >= t && i - t < m) Cb[(i - t) + (m - 1) * LDC] = val;
+                            }
+                        }
+                        if (hasB && !cu)
+                            for (int i = tid - 32; i < m; i += NT - 32) Cb[i + (m - 1) * LDC] = ys[t + i];
+                    }
+                    __syncthreads();
+                    K1_TICK(7);
+                    tau = scal[0];
+                    // (A(b0:i2, jb), B(b0:i1-1, cB) and the record are stored by the RQ's idle warps)
+                } else {
                 __syncthreads();
                 K1_TICK(2);
                 // ---- (S3) left reflector Q_k^j on A(i1:i2,jb) ----------------------------------
                 if (warp == 0) {
-                    S tau;
+                    S tq;
                     double beta;
-                    warp_larfg(m, xcol + t, vq, tau, beta);
+                    warp_larfg(m, xcol + t, vq, tq, beta);
                     if (lane == 0) {
-                        scal[0] = tau;
+                        scal[0] = tq;
                         scal[1] = S(beta);
                     }
                 }
                 __syncthreads();
                 K1_TICK(7);
-                const S tau = scal[0];
+                tau = scal[0];
                 {
                     const S betaS = scal[1];
                     for (int i = tid; i < nx; i += NT) {
@@ -883,8 +965,9 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
                     for (int c = tid; c < m; c += NT) qr[c] = vq[c];
                     if (tid == 0) qr[r] = tau;
                 }
-                if constexpr (!MK) __syncthreads();  // (the dense path's Q^*B reads none of it)
+                __syncthreads();
                 K1_TICK(8);
+                }
                 // ---- (S4) B block <- Q^* B block (warps 0..NW/2-1) || T column t (others) ------
                 if constexpr (MK) {
                     // m <= 32: a group of G lanes per column, one element per lane
@@ -969,8 +1052,21 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
                     pf_next = true;
                 }
                 if constexpr (MK) {
-                    // the idle warps form M_{t+1}(k) = (Q_k^j)^* M_t(k) for sweep t+1 (in place in Mg)
                     constexpr int RQT = rq_nthr<S, MAXM>();
+                    if (tid >= RQT) {  // the step's stores of A(b0:i2, jb), B(b0:i1-1, cB), record
+                        const int nth = NT - RQT, me = tid - RQT;
+                        const S betaS = scal[1];
+                        for (int i = me; i < nx; i += nth) {
+                            const S val = (i < t) ? mtmp[i] : ((i == t) ? betaS : S(0.0));  // exact zeros (c5)
+                            IDX(a.A, a.lda, b0 + i, jb) = val;
+                        }
+                        if (hasB)
+                            for (int i = me; i < t; i += nth) IDX(a.B, a.ldb, b0 + i, cB) = mtmp[L + i];
+                        S* qr = a.Qr + ((int64_t)t * K + k) * (r + 1);
+                        for (int c = me; c < m; c += nth) qr[c] = vq[c];
+                        if (me == 0) qr[r] = tau;
+                    }
+                    // the idle warps form M_{t+1}(k) = (Q_k^j)^* M_t(k) for sweep t+1 (in place in Mg)
                     if (t + 1 < qp && tid >= RQT) {
                         const int nth = NT - RQT, me = tid - RQT, mw = me >> 5, nw = nth >> 5;
                         const int Ln = min(j + (k + 1) * r, n) - b0 + 1;
@@ -987,7 +1083,7 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
                                 d1 += conj_mul(vq[p2 + 1], base(t + p2 + 1, c));
                             }
                             if (p2 < m) d0 += conj_mul(vq[p2], base(t + p2, c));
-                            mtmp[c] = (d0 + d1) * ctau;
+                            wx[c] = (d0 + d1) * ctau;
                         }
                         named_bar(3, nth);
                         S* dst = a.Mg + (int64_t)k * a.mst;
@@ -996,7 +1092,7 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
                             const S vi = upd ? vq[i - t] : S(0.0);
                             for (int c = lane; c < Ln; c += 32) {
                                 S val = base(i, c);
-                                if (upd) val -= vi * mtmp[c];
+                                if (upd) val -= vi * wx[c];
                                 dst[(size_t)i * MLD + c] = val;
                             }
                         }
@@ -1017,7 +1113,7 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
                     // caught-up rows b0..i1-1 of column i2 are also rows of the staged B strip
                     for (int i = tid - 32; i < t && i < L; i += NT - 32) {
                         const int rr = (b0 + i) - i4;
-                        if (rr >= 0 && rr < stB) strip[(stA + rr) * SLD + (m - 1)] = ys[i];
+                        if (rr >= 0 && rr < stB) strip[(stA + rr) * SLD + (m - 1)] = MK ? mtmp[L + i] : ys[i];
                     }
                 }
                 __syncthreads();
@@ -1107,6 +1203,6 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
         pt[11] += 1;  // step count (not a time slot)
     }
     if (a.prof && tid == 0 && (a.prof_t0 < 0 || t == a.prof_t0))
-        for (int i = 0; i < 12; ++i) atomicAdd((unsigned long long*)&a.prof[i], (unsigned long long)pt[i]);
+        for (int i = 0; i < 16; ++i) atomicAdd((unsigned long long*)&a.prof[i], (unsigned long long)pt[i]);
 #undef K1_TICK
 }

@@ -189,7 +189,7 @@ struct Workspace {
     S *U[NUV] = {}, *V[NUV] = {}, *MU[NUV] = {}, *MV[NUV] = {}, *Zr = nullptr, *Qr = nullptr, *Tr = nullptr, *Mg = nullptr;
     int* prog = nullptr;
     long long* k1prof = nullptr;
-    long long k1prof_host[12] = {0};
+    long long k1prof_host[16] = {0};
     cudaStream_t side = nullptr;
     cudaEvent_t ev_uv[NUV] = {}, ev_qz[NUV] = {};
     bool async = true;
@@ -217,8 +217,8 @@ struct Workspace {
         if (chase_dense_catchup<S>(p.r)) CK(mal((void**)&Mg, (size_t)p.Kmax * mcatch_st(p.q, p.r) * sizeof(S)));
         CK(mal((void**)&prog, (size_t)(5 * p.q + 2) * sizeof(int)));
         if (k1p) {
-            CK(mal((void**)&k1prof, 12 * sizeof(long long)));
-            CK(cudaMemsetAsync(k1prof, 0, 12 * sizeof(long long), stream));
+            CK(mal((void**)&k1prof, 16 * sizeof(long long)));
+            CK(cudaMemsetAsync(k1prof, 0, 16 * sizeof(long long), stream));
         }
         if (p.qz()) {
             int lo = 0, hi = 0;
@@ -263,14 +263,19 @@ struct Workspace {
 };
 
 void print_k1prof(const long long* h) {
-    const char* nm[11] = {"wait", "loads", "catchup", "QB+T", "larfgZ", "strip", "RQ", "larfgQ", "writes", "waitH", "s10"};
+    // slots 0..10 and 12..15 are cycles of thread 0 of the profiled sweeps; slot 11 counts steps
+    const char* nm[16] = {"wait", "loads", "catchup", "QB+T", "larfgZ", "strip", "RQ", "larfgQ", "writes", "waitH",
+                          "s10", "", "s12", "s13", "s14", "s15"};
     double tot = 0;
-    for (int i = 0; i < 11; ++i) tot += (double)h[i];
-    const double steps = h[11] > 0 ? (double)h[11] : 1.0;  // slot 11 counts steps
+    for (int i = 0; i < 16; ++i)
+        if (i != 11) tot += (double)h[i];
+    const double steps = h[11] > 0 ? (double)h[11] : 1.0;
     fprintf(stderr, "K1 cycles (sum over CTAs):");
-    for (int i = 0; i < 11; ++i) fprintf(stderr, " %s=%.1f%%", nm[i], 100.0 * h[i] / (tot > 0 ? tot : 1));
+    for (int i = 0; i < 16; ++i)
+        if (i != 11 && h[i]) fprintf(stderr, " %s=%.1f%%", nm[i], 100.0 * h[i] / (tot > 0 ? tot : 1));
     fprintf(stderr, " total=%.3g steps=%.0f\nK1 cycles per step:", tot, steps);
-    for (int i = 0; i < 11; ++i) fprintf(stderr, " %s=%.0f", nm[i], h[i] / steps);
+    for (int i = 0; i < 16; ++i)
+        if (i != 11 && h[i]) fprintf(stderr, " %s=%.0f", nm[i], h[i] / steps);
     fprintf(stderr, " all=%.0f\n", tot / steps);
 }
 
