@@ -156,7 +156,10 @@ struct RQCfg {
     static constexpr int NSB = (E + SB - 1) / SB;
     static constexpr int ROWT = MAXM * LPR;
     static constexpr int NA = (ROWT < 32) ? 32 : ROWT;
-    static constexpr bool NOB = MAXM > 64;
+#ifndef HT_RQ_NOB_ABOVE
+#define HT_RQ_NOB_ABOVE 64
+#endif
+    static constexpr bool NOB = MAXM > HT_RQ_NOB_ABOVE;
     static constexpr int NTHR = NOB ? NA : 2 * NA;
     static constexpr int PLD = LPR * NSB * SB + 4;  // ring slot: pivot row (de-interleaved) + K1, K2
 };
@@ -550,6 +553,7 @@ __device__ __forceinline__ void far_strip_helper(const ChaseArgs<S>& a, int t, i
     constexpr int SPR = (MAXM * (int)sizeof(S) > 256) ? MAXM * (int)sizeof(S) / 256 : 1;
     constexpr int CPR = MAXM / SPR;
     const int part = tid % SPR, c0 = part * CPR;
+    long long hw = 0, hx = 0, tc = clock64();  // profile: cycles waiting / working (helper 0)
     for (int k = 0; k < kcount; ++k) {
         if (tid == 0) {
             if (ld_acquire(&a.prog[t]) < k + 1)
@@ -564,6 +568,12 @@ __device__ __forceinline__ void far_strip_helper(const ChaseArgs<S>& a, int t, i
             if (t > 0) (void)ld_acquire(&hprog[(t - 1) * H + h]);
         }
         __syncthreads();
+        if (a.prof && tid == 0) {
+            (void)*(volatile S*)sm;
+            const long long now = clock64();
+            hw += now - tc;
+            tc = now;
+        }
         const int i1 = j + k * r + 1;
         const int i2 = min(j + (k + 1) * r, n);
         const int i3 = min(j + (k + 2) * r, n);
@@ -573,7 +583,7 @@ __device__ __forceinline__ void far_strip_helper(const ChaseArgs<S>& a, int t, i
         const int nAf = max(0, min(cF, i3 + 1) - i4), nBf = max(0, min(cF, i2 + 1) - i4);
         if (m >= 2 && nAf + nBf > 0) {
             const S* rec = a.Zr + ((int64_t)t * K + k) * (r + 1);
-            for (int c = tid; c < m; c += NT) zv[c] = ldcg(rec + c);
+            for (int c = tid; c < MAXM; c += NT) zv[c] = (c < m) ? ldcg(rec + c) : S(0.0);  // (zero pad)
             if (tid == 0) zv[MAXM] = ldcg(rec + r);
             __syncthreads();
             const S sig = zv[MAXM];
@@ -594,13 +604,15 @@ __device__ __forceinline__ void far_strip_helper(const ChaseArgs<S>& a, int t, i
                         S v[CPR];
                         S s0 = S(0.0), s1 = S(0.0);
                         if (act) {
+                            // all loads first: an FMA waiting on its load would hold back the
+                            // next load's issue (in-order issue), one memory latency per element
 #pragma unroll
-                            for (int c = 0; c < CPR; ++c)
-                                if (c0 + c < m) {
-                                    v[c] = ldcg(gp + (c0 + c) * ld);
-                                    if (c & 1) s1 = fma_s(v[c], zv[c0 + c], s1);
-                                    else s0 = fma_s(v[c], zv[c0 + c], s0);
-                                }
+                            for (int c = 0; c < CPR; ++c) v[c] = (c0 + c < m) ? ldcg(gp + (c0 + c) * ld) : S(0.0);
+#pragma unroll
+                            for (int c = 0; c < CPR; ++c) {
+                                if (c & 1) s1 = fma_s(v[c], zv[c0 + c], s1);
+                                else s0 = fma_s(v[c], zv[c0 + c], s0);
+                            }
                         }
                         S sdot = s0 + s1;
                         if constexpr (SPR > 1) {
@@ -622,6 +634,15 @@ __device__ __forceinline__ void far_strip_helper(const ChaseArgs<S>& a, int t, i
             __threadfence();
             st_release(&hprog[t * H + h], k + 1);
         }
+        if (a.prof && tid == 0) {
+            const long long now = clock64();
+            hx += now - tc;
+            tc = now;
+        }
+    }
+    if (a.prof && tid == 0 && h == 0 && (a.prof_t0 < 0 || t == a.prof_t0)) {
+        atomicAdd((unsigned long long*)&a.prof[14], (unsigned long long)hw);
+        atomicAdd((unsigned long long*)&a.prof[15], (unsigned long long)hx);
     }
 }
 

@@ -265,9 +265,9 @@ struct Workspace {
 void print_k1prof(const long long* h) {
     // slots 0..10 and 12..15 are cycles of thread 0 of the profiled sweeps; slot 11 counts steps
     const char* nm[16] = {"wait", "loads", "catchup", "QB+T", "larfgZ", "strip", "RQ", "larfgQ", "writes", "waitH",
-                          "s10", "", "s12", "s13", "s14", "s15"};
+                          "s10", "", "s12", "s13", "hwait", "hwork"};
     double tot = 0;
-    for (int i = 0; i < 16; ++i)
+    for (int i = 0; i < 14; ++i)  // (14, 15: the helper's own wait / work, not part of the sweep's)
         if (i != 11) tot += (double)h[i];
     const double steps = h[11] > 0 ? (double)h[11] : 1.0;
     fprintf(stderr, "K1 cycles (sum over CTAs):");
