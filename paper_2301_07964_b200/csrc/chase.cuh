@@ -150,7 +150,10 @@ __device__ __forceinline__ S larfg_reg(S xv, int m, S& tau, double& beta) {
 // Q~^* e1 = H_{m-1}...H_0 e1 is formed afterwards by one warp from the stored reflectors.
 template <typename S, int MAXM>
 struct RQCfg {
-    static constexpr int LPR = (MAXM >= 16) ? 2 : 1;
+#ifndef HT_RQ_LPR64
+#define HT_RQ_LPR64 2
+#endif
+    static constexpr int LPR = (MAXM == 64) ? HT_RQ_LPR64 : ((MAXM >= 16) ? 2 : 1);
     static constexpr int E = MAXM / LPR;
     static constexpr int SB = 8;
     static constexpr int NSB = (E + SB - 1) / SB;

@@ -45,7 +45,7 @@ int main() {
         if (m == 8) { cudaFuncSetAttribute(bench<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100000); bench<8><<<1, 256, 100000>>>(C, out, cyc, m, 20); }
         if (m == 16) { cudaFuncSetAttribute(bench<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100000); bench<16><<<1, 256, 100000>>>(C, out, cyc, m, 20); }
         if (m == 32) { cudaFuncSetAttribute(bench<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100000); bench<32><<<1, 256, 100000>>>(C, out, cyc, m, 20); }
-        if (m == 64) { cudaFuncSetAttribute(bench<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100000); bench<64><<<1, 256, 100000>>>(C, out, cyc, m, 20); }
+        if (m == 64) { cudaFuncSetAttribute(bench<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100000); bench<64><<<1, rq_nthr<double, 64>() > 256 ? rq_nthr<double, 64>() : 256, 100000>>>(C, out, cyc, m, 20); }
         cudaDeviceSynchronize();
         // residual of rows 1..m-1 of C u (must vanish) and |u|
         double res = 0, nu = 0, nc = 0;
