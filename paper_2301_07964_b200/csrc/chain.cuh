@@ -45,7 +45,22 @@ struct ChainParams {
     int njobs;
     const S* Zr;  // staircase reflectors: (qp*K) records of (r+1)
     int P;        // window merge factor (1 = off): steps cover P windows where the tile is fully inside
+    int spread;   // > 0 (H/T, two jobs of equal tile count): block order longest chain first (see below)
 };
+
+// H/T chains are latency-bound by their longest tiles (right updates: the top row tiles walk
+// every window; left updates: the rightmost column tiles).  With spread = G (the SM count) the
+// first G blocks -- one per SM in the first dispatch round -- take the G longest tiles (H and T
+// interleaved) and block G + x takes the x-th SHORTEST, so an SM's second tile finishes early and
+// leaves the long chain alone on the SM.  Returns (job, tile) of block b.
+inline __host__ __device__ int chain_spread(int nsm) { return nsm > 0 ? nsm : 148; }
+__device__ __forceinline__ void chain_order(int b, int total, int spread, bool longest_low, int nt, int& job,
+                                            int& tile) {
+    const int rank = (spread > 0 && b >= spread) ? total - 1 - (b - spread) : b;
+    job = rank & 1;
+    const int tr = rank >> 1;
+    tile = longest_low ? tr : nt - 1 - tr;
+}
 
 constexpr int CH_BM = 32;      // tile rows per CTA (one warp row of 4 m8 tiles)
 constexpr int CH_KC = 16;      // k rows per ring chunk
@@ -163,7 +178,10 @@ __device__ __forceinline__ bool chain_tile(const ChainParams<S>& P, int bid, uns
 
     // ---- which job / tile ----
     int jb_ = 0;
-    if (P.njobs > 1 && bid >= P.job[0].ntiles) {
+    if (P.spread > 0 && P.njobs == 2 && P.job[0].ntiles == P.job[1].ntiles) {
+        const int m0 = P.job[0].mode;
+        chain_order(bid, 2 * P.job[0].ntiles, P.spread, m0 == CM_AB_RIGHT, P.job[0].ntiles, jb_, bid);
+    } else if (P.njobs > 1 && bid >= P.job[0].ntiles) {
         bid -= P.job[0].ntiles;
         jb_ = 1;
     }
@@ -330,24 +348,28 @@ __device__ __forceinline__ bool chain_tile(const ChainParams<S>& P, int bid, uns
             __syncthreads();  // everyone is past chunk cseq-1: its stage may be refilled
             issue_next();
             const S* Bs = ring + (size_t)s * CH_KC * LDB;
+            if (wn * (WP / WN) < wk) {  // warp-uniform: this warp's columns exist in the step
+                // the chunk's fragments first (their shared-memory latencies overlap), then the MMAs
+                constexpr int KS = CH_KC / 4;
+                S a[KS][MT], b[KS][NTL];
 #pragma unroll
-            for (int kk = 0; kk < CH_KC; kk += 4) {
-                const int kl = ch * CH_KC + kk + (lane & 3);  // window-local column (K index)
-                int pos = p + kl;
-                if (pos >= CIRC) pos -= CIRC;
-                if (pos >= CIRC) pos -= CIRC;
-                S a[MT], b[NTL];
+                for (int ks = 0; ks < KS; ++ks) {
+                    const int kl = ch * CH_KC + ks * 4 + (lane & 3);  // window-local column (K index)
+                    int pos = p + kl;
+                    if (pos >= CIRC) pos -= CIRC;
+                    if (pos >= CIRC) pos -= CIRC;
 #pragma unroll
-                for (int mt = 0; mt < MT; ++mt) a[mt] = X[pos * CH_LDX + rowb + mt * 8];
+                    for (int mt = 0; mt < MT; ++mt) a[ks][mt] = X[pos * CH_LDX + rowb + mt * 8];
 #pragma unroll
-                for (int nt = 0; nt < NTL; ++nt)
-                    b[nt] = maybe_conj(Bs[(kk + (lane & 3)) * LDB + colb + nt * 8], trans);
-                if (wn * (WP / WN) < wk) {  // warp-uniform: this warp's columns exist in the step
+                    for (int nt = 0; nt < NTL; ++nt)
+                        b[ks][nt] = maybe_conj(Bs[(ks * 4 + (lane & 3)) * LDB + colb + nt * 8], trans);
+                }
+#pragma unroll
+                for (int ks = 0; ks < KS; ++ks)
 #pragma unroll
                     for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
-                        for (int nt = 0; nt < NTL; ++nt) mma_step(acc[mt][nt], a[mt], b[nt]);
-                }
+                        for (int nt = 0; nt < NTL; ++nt) mma_step(acc[mt][nt], a[ks][mt], b[ks][nt]);
             }
             ++cseq;
         }

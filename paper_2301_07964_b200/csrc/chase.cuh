@@ -1010,27 +1010,40 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
                         }
                     }
                 } else if (warp < NW / 2) {
+                    // warps 0..NW/2-1: warp per column, RPL rows per lane, U columns in flight
+                    // (their shuffle reductions interleave)
                     if (!is_zero(tau)) {
                         const S ctau = conjv(tau);
-                        if (m <= 32) {  // warp 0: lane per column, no reductions
-                            if (warp == 0 && lane < m) {
-                                S* col = Cb + lane * LDC;
-                                S s0 = S(0.0), s1 = S(0.0);
-                                int i = 0;
-                                for (; i + 1 < m; i += 2) {
-                                    s0 += conj_mul(vq[i], col[i]);
-                                    s1 += conj_mul(vq[i + 1], col[i + 1]);
+                        constexpr int RPL = (MAXM + 31) / 32, U = 4, WG = NW / 2;
+                        S vr[RPL];
+#pragma unroll
+                        for (int rr = 0; rr < RPL; ++rr) vr[rr] = (lane + 32 * rr < m) ? vq[lane + 32 * rr] : S(0.0);
+                        for (int cb = warp; cb < m; cb += WG * U) {
+                            S e[U][RPL], d[U];
+#pragma unroll
+                            for (int u = 0; u < U; ++u) {
+                                const int c = cb + u * WG;
+                                d[u] = S(0.0);
+#pragma unroll
+                                for (int rr = 0; rr < RPL; ++rr) {
+                                    const int i = lane + 32 * rr;
+                                    e[u][rr] = (c < m && i < m) ? Cb[i + c * LDC] : S(0.0);
+                                    d[u] += conj_mul(vr[rr], e[u][rr]);
                                 }
-                                if (i < m) s0 += conj_mul(vq[i], col[i]);
-                                const S sc = (s0 + s1) * ctau;
-                                for (i = 0; i < m; ++i) col[i] -= vq[i] * sc;
                             }
-                        } else {
-                            for (int c = warp; c < m; c += NW / 2) {
-                                S s = S(0.0);
-                                for (int i = lane; i < m; i += 32) s += conj_mul(vq[i], Cb[i + c * LDC]);
-                                s = warp_sum(s) * ctau;
-                                for (int i = lane; i < m; i += 32) Cb[i + c * LDC] -= vq[i] * s;
+#pragma unroll
+                            for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+                                for (int u = 0; u < U; ++u) d[u] += shfl_xor(d[u], o);
+#pragma unroll
+                            for (int u = 0; u < U; ++u) {
+                                const int c = cb + u * WG;
+                                const S sc = d[u] * ctau;
+#pragma unroll
+                                for (int rr = 0; rr < RPL; ++rr) {
+                                    const int i = lane + 32 * rr;
+                                    if (c < m && i < m) Cb[i + c * LDC] = e[u][rr] - vr[rr] * sc;
+                                }
                             }
                         }
                     }
@@ -1040,8 +1053,17 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
                     for (int s = me; s < t; s += hn) {
                         const S* v = rec + (size_t)s * (r + 1);
                         const int ms = min(r, n - (j1 + s + k * r));
-                        S d = S(0.0);
-                        for (int ii = t; ii < s + ms && ii - t < m; ++ii) d += conj_mul(v[ii - s], vq[ii - t]);
+                        const int hi = min(s + ms, t + m);
+                        S d0 = S(0.0), d1 = S(0.0), d2 = S(0.0), d3 = S(0.0);
+                        int ii = t;
+                        for (; ii + 3 < hi; ii += 4) {
+                            d0 += conj_mul(v[ii - s], vq[ii - t]);
+                            d1 += conj_mul(v[ii + 1 - s], vq[ii + 1 - t]);
+                            d2 += conj_mul(v[ii + 2 - s], vq[ii + 2 - t]);
+                            d3 += conj_mul(v[ii + 3 - s], vq[ii + 3 - t]);
+                        }
+                        for (; ii < hi; ++ii) d0 += conj_mul(v[ii - s], vq[ii - t]);
+                        S d = (d0 + d1) + (d2 + d3);
                         if (is_zero(v[r])) d = S(0.0);
                         wu[s] = d;
                     }

@@ -167,6 +167,7 @@ struct Plan {
     int rank = 0, nranks = 1, root = 0, emul = 1;
     int helpers = 1;  // far-strip helper CTAs per sweep in the chase
     int P = 1;        // window merge factor of the apply chains (K2m)
+    int nsm = 148;    // SMs (longest-chain-first tile order of the H/T chains)
     size_t mrg_bytes = 0;
     bool is_root() const { return comm == nullptr || rank == root; }
     bool qz() const { return Q || Z; }
@@ -389,10 +390,12 @@ int enqueue_groups(const Plan<S>& p, Workspace<S>& ws, cudaStream_t stream, bool
         const int tiles = (n + CH_BM - 1) / CH_BM;
         if (root) {
             ChainParams<S> pr{n, r, qp, j1, K, {{p.H, p.ldh, ws.V[bsel], ws.MV[bsel], CM_AB_RIGHT, 0, tiles, 0},
-                                                {p.T, p.ldt, ws.V[bsel], ws.MV[bsel], CM_AB_RIGHT, 0, tiles, 0}}, 2, ws.Zr, p.P};
+                                                {p.T, p.ldt, ws.V[bsel], ws.MV[bsel], CM_AB_RIGHT, 0, tiles, 0}}, 2, ws.Zr, p.P,
+                              chain_spread(p.nsm)};
             if (int rc = chain<S>(pr, WP, 2 * tiles, r, q, stream)) return rc;
             ChainParams<S> pl{n, r, qp, j1, K, {{p.H, p.ldh, ws.U[bsel], ws.MU[bsel], CM_A_LEFT, 1, tiles, 0},
-                                                {p.T, p.ldt, ws.U[bsel], ws.MU[bsel], CM_B_LEFT, 1, tiles, 0}}, 2, ws.Zr, p.P};
+                                                {p.T, p.ldt, ws.U[bsel], ws.MU[bsel], CM_B_LEFT, 1, tiles, 0}}, 2, ws.Zr, p.P,
+                              chain_spread(p.nsm)};
             if (int rc = chain<S>(pl, WP, 2 * tiles, r, q, stream)) return rc;
             g_last_launches += 2;
         }
@@ -603,6 +606,7 @@ int run(int64_t n64, int64_t r64, S* H, int64_t ldh, S* T, int64_t ldt, S* Q, in
                std::max(8, nsm - (1 + helpers) * q)};
     pl.helpers = helpers;
     pl.P = PM;
+    pl.nsm = nsm;
     pl.mrg_bytes = mrg_bytes;
     if (comm) {
         pl.comm = comm;
