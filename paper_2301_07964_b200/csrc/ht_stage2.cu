@@ -576,7 +576,9 @@ int run(int64_t n64, int64_t r64, S* H, int64_t ldh, S* T, int64_t ldt, S* Q, in
     const int WP = (Wm + 31) / 32 * 32;  // padded window order (DMMA tiles, ring chunks)
     const int LDB = chain_ldb(WP);
     const int Kmax = 1 + (n - 1 - 2) / r;
-    const int chase_budget = 200 * 1024;
+    // shared memory of a chase CTA; what the fixed buffers leave goes to staged strip rows
+    // (HT_CHASE_SMEM_KB overrides; 224 KB measured no faster than 200 at r = 32, 64)
+    const int chase_budget = (getenv("HT_CHASE_SMEM_KB") ? atoi(getenv("HT_CHASE_SMEM_KB")) : 200) * 1024;
     const size_t chase_base = chase_smem_elems<S>(r, q, 0) * sizeof(S);
     const int strip_cap = (int)std::max<int64_t>(0, ((int64_t)chase_budget - (int64_t)chase_base) /
                                                         (int64_t)((r + 1) * sizeof(S)));

@@ -1,5 +1,9 @@
-cd $GRAFT_REPO_ROOT
-./tools/rq_bench > gpurun_out/rq_bench.log 2>&1
-timeout 600 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo rc=$? >> gpurun_out/pytest_gpu.log
-timeout 300 python tools/k1prof.py 4096 16 16 > gpurun_out/plain_k1.log 2>&1 && \
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:chase -s 100 -c 1 -o gpurun_out/prof_chase_c2_v3 python tools/k1prof.py 4096 16 16 > gpurun_out/ncu_chase.log 2>&1
+#!/bin/bash
+cd "$GRAFT_REPO_ROOT" || exit 1
+rm -f gpurun_out/ht.log
+for kb in 200 224; do
+ for a in "8192 64 32" "8192 32 16 c" "4096 16 32"; do
+  echo "== $a kb=$kb" >> gpurun_out/ht.log
+  HT_CHASE_SMEM_KB=$kb timeout 300 python tools/k1prof.py $a 2>&1 | grep wall | tail -1 >> gpurun_out/ht.log
+ done
+done
