@@ -1,9 +1,14 @@
 #!/bin/bash
 cd "$GRAFT_REPO_ROOT" || exit 1
-rm -f gpurun_out/ht.log
-for kb in 200 224; do
- for a in "8192 64 32" "8192 32 16 c" "4096 16 32"; do
-  echo "== $a kb=$kb" >> gpurun_out/ht.log
-  HT_CHASE_SMEM_KB=$kb timeout 300 python tools/k1prof.py $a 2>&1 | grep wall | tail -1 >> gpurun_out/ht.log
- done
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_gpu.log
+rm -f gpurun_out/lov.log
+for c in 2 3; do
+  for v in 0 1; do
+    echo "== config $c HT_NO_LOVERLAP=$v" >> gpurun_out/lov.log
+    if [ $v = 1 ]; then export HT_NO_LOVERLAP=1; else unset HT_NO_LOVERLAP; fi
+    timeout 300 python bench.py --config $c --steps 2 --warmup 3 --no-cpu --no-e2e 2>>gpurun_out/lov.err | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['ms_per_step'], d['value'])" >> gpurun_out/lov.log 2>&1
+  done
 done
+unset HT_NO_LOVERLAP
+echo done
