@@ -44,6 +44,21 @@ def _peaks():
         return {}
 
 
+def _ncu_traffic(kernel, n, r, q):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel` from the committed
+    `ncu --set full` capture summary (profiles/ncu_traffic.json), when it was taken on this
+    workload; else None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            d = json.load(f)
+        e = d[kernel]
+        if (e["n"], e["r"], e["q"]) == (n, r, q):
+            return e["bytes_per_launch"]
+    except Exception:
+        pass
+    return None
+
+
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons DURING the timed region (B200_PROFILING.md)."""
 
@@ -254,14 +269,14 @@ def main():
     dfma = ht.probe_dfma_tflops(20000)
     ach_k1 = (rq + band) / (brk["chase"] * 1e-3) / 1e12
     roof_k1 = {"kernel": "chase_kernel (K1)", "bound": "alu", "achieved": ach_k1, "peak": dfma, "unit": "TFLOP/s",
-               "frac": ach_k1 / dfma, "traffic": None,
+               "frac": ach_k1 / dfma, "traffic": _ncu_traffic("chase_kernel", n, r, q),
                "peak_source": "measured DFMA probe (ht_probe_dfma_tflops) on this GPU; MEASURED_PEAKS.json has no FP64 figure",
                "algorithmic": "RQ (2/3)r^2n^2 + generate band 2r(q+2)n^2 flops per call (a latency-bound chain)",
                "share_of_step": brk["chase"] / ms_step}
     ht_cnt = (4.03 if not cplx else 4.03 * 4) * n ** 3  # counted H,T update flops (left + right) [V2]
     ach_ht = ht_cnt / (brk["ht_updates"] * 1e-3) / 1e12
     roof_ht = {"kernel": "chain_kernel, H/T right + left (K3/K4)", "bound": "tensor", "achieved": ach_ht, "peak": dmma,
-               "unit": "TFLOP/s", "frac": ach_ht / dmma, "traffic": None,
+               "unit": "TFLOP/s", "frac": ach_ht / dmma, "traffic": _ncu_traffic("chain_kernel", n, r, q),
                "peak_source": "measured DMMA (mma.sync f64) probe on this GPU; MEASURED_PEAKS.json has no FP64 figure",
                "algorithmic": "counted H,T update flops 4.03n^3 per call (x4 complex); dense U/V execute (q+r-1)^2/(2qr) x",
                "share_of_step": brk["ht_updates"] / ms_step}

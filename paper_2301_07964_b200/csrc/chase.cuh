@@ -968,7 +968,12 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
                 if (warp == 0) {
                     S tq;
                     double beta;
-                    warp_larfg(m, xcol + t, vq, tq, beta);
+                    if constexpr (MAXM <= 32) {
+                        const S vl = larfg_reg(lane < m ? xcol[t + lane] : S(0.0), m, tq, beta);
+                        if (lane < m) vq[lane] = vl;
+                    } else {
+                        warp_larfg(m, xcol + t, vq, tq, beta);
+                    }
                     if (lane == 0) {
                         scal[0] = tq;
                         scal[1] = S(beta);
@@ -1153,7 +1158,12 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
                 if (warp == 0) {
                     S sig;
                     double b2;
-                    warp_larfg(m, uu, vz, sig, b2);
+                    if constexpr (MAXM <= 32) {  // register form (fast rsqrt / reciprocal)
+                        const S vl = larfg_reg(lane < m ? uu[lane] : S(0.0), m, sig, b2);
+                        if (lane < m) vz[lane] = vl;
+                    } else {
+                        warp_larfg(m, uu, vz, sig, b2);
+                    }
                     if (lane == 0) scal[2] = sig;
                 } else if (hasB && cu) {
                     // caught-up rows b0..i1-1 of column i2 are also rows of the staged B strip
