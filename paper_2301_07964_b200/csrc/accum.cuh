@@ -15,6 +15,7 @@
 template <typename S>
 struct AccumArgs {
     int n, r, qp, j1, K, WP, LDB;
+    int pre;  // 1: all records of the window staged at once (else one at a time: large w)
     const S* Qr;
     const S* Zr;
     S* U;
@@ -22,9 +23,9 @@ struct AccumArgs {
 };
 
 template <typename S>
-__host__ __device__ inline size_t accum_smem_bytes(int r, int qp) {
+__host__ __device__ inline size_t accum_smem_bytes(int r, int qp, bool pre) {
     const int w = qp + r - 1;
-    return ((size_t)w * (w | 1) + (size_t)(r + 8)) * sizeof(S);
+    return ((size_t)w * (w | 1) + (pre ? (size_t)qp * (r + 1) : (size_t)(r + 1))) * sizeof(S);
 }
 
 template <typename S, int NT>
@@ -39,20 +40,26 @@ __global__ void __launch_bounds__(NT) accum_kernel(AccumArgs<S> a) {
     const int w = qp + r - 1;
     const int wk = min(w, n - (j1 + k * r + 1) + 1);
     const int LX = wk | 1;  // odd row stride: thread-per-row access is conflict-free
-    S* vs = X + (size_t)wk * LX;
+    S* recs = X + (size_t)wk * LX;  // all qp records of the window, loaded at once
     const int tid = threadIdx.x;
     for (int e = tid; e < wk * LX; e += NT) {
         const int l = e / LX, c = e % LX;
         X[e] = S(l == c ? 1.0 : 0.0);
     }
+    if (a.pre)
+        for (int t = tid / 32; t < qp; t += NT / 32)  // warp per record (one latency for all of them)
+            for (int c = tid % 32; c <= r; c += 32) recs[(size_t)t * (r + 1) + c] = R[((size_t)t * K + k) * (r + 1) + c];
     __syncthreads();
     for (int t = 0; t < qp; ++t) {
-        const S* rec = R + ((size_t)t * K + k) * (r + 1);
-        const S tau = rec[r];
+        const S* vs = recs + (a.pre ? (size_t)t * (r + 1) : 0);
+        if (!a.pre) {
+            const S* rec = R + ((size_t)t * K + k) * (r + 1);
+            for (int c = tid; c <= r; c += NT) recs[c] = rec[c];
+            __syncthreads();
+        }
+        const S tau = vs[r];
         if (is_zero(tau)) continue;  // uniform across the block
         const int m = min(r, min(n - (j1 + t + k * r), wk - t));
-        for (int c = tid; c < m; c += NT) vs[c] = rec[c];
-        __syncthreads();
         const int rows = min(t + m, wk);
         for (int l = tid; l < rows; l += NT) {
             S* xr = X + (size_t)l * LX + t;
@@ -93,7 +100,7 @@ struct MergeArgs {
 
 template <typename S>
 __host__ __device__ inline size_t merge_smem_bytes(int W, int w) {
-    return (2 * (size_t)W * (W | 1) + (size_t)w * (w | 1)) * sizeof(S);
+    return ((size_t)W * (W | 1) + (size_t)W * (w + 4) + (size_t)w * (w + 4)) * sizeof(S);
 }
 
 template <typename S, int NT>
@@ -109,10 +116,11 @@ __global__ void __launch_bounds__(NT) merge_kernel(MergeArgs<S> a) {
     const int c0 = j1 + klo * r + 1;
     const int W = min(qp + (khi - klo + 1) * r - 1, n - c0 + 1);
     const int LM = W | 1;
+    // M (W x LM); Tm = M(:, o:o+wk) V'_k (W x LT), then copied back; Vs = the window block (w x LT)
+    const int LT = w + 4;
     S* M = reinterpret_cast<S*>(smraw);
-    S* M2 = M + (size_t)W * LM;
-    S* Vs = M2 + (size_t)W * LM;  // the current window block (w x (w|1))
-    const int LV = w | 1;
+    S* Tm = M + (size_t)W * LM;
+    S* Vs = Tm + (size_t)W * LT;
     const int tid = threadIdx.x;
     // M = V'_khi (identity outside its columns)
     {
@@ -129,39 +137,49 @@ __global__ void __launch_bounds__(NT) merge_kernel(MergeArgs<S> a) {
             M[e] = v;
         }
     }
-    __syncthreads();
     for (int k = khi - 1; k >= klo; --k) {  // M <- M V'_k (columns o .. o+wk)
         const int o = (k - klo) * r;
         const int wk = min(w, n - (j1 + k * r + 1) + 1);
         const S* B = Blk + (size_t)k * a.WP * a.LDB;
         for (int e = tid; e < wk * wk; e += NT) {
             const int l = e / wk, c = e % wk;
-            Vs[(size_t)l * LV + c] = B[(size_t)l * a.LDB + c];
+            Vs[(size_t)l * LT + c] = B[(size_t)l * a.LDB + c];
         }
         __syncthreads();
-        for (int e = tid; e < W * LM; e += NT) {
-            const int l = e / LM, c = e % LM;
-            S v = M[e];
-            if (c >= o && c < o + wk) {
-                S s0 = S(0.0), s1 = S(0.0), s2 = S(0.0), s3 = S(0.0);
-                const S* mr = M + (size_t)l * LM + o;
-                const S* vc = Vs + (c - o);
-                int cc = 0;
-                for (; cc + 3 < wk; cc += 4) {
-                    s0 = fma_s(mr[cc], vc[(size_t)cc * LV], s0);
-                    s1 = fma_s(mr[cc + 1], vc[(size_t)(cc + 1) * LV], s1);
-                    s2 = fma_s(mr[cc + 2], vc[(size_t)(cc + 2) * LV], s2);
-                    s3 = fma_s(mr[cc + 3], vc[(size_t)(cc + 3) * LV], s3);
-                }
-                for (; cc < wk; ++cc) s0 = fma_s(mr[cc], vc[(size_t)cc * LV], s0);
-                v = (s0 + s1) + (s2 + s3);
+        // register tiles of 4 rows x 4 columns: 8 shared loads per 16 FMAs (lanes of a warp share
+        // the row tile: the M loads broadcast, the Vs loads are consecutive)
+        const int nct = (wk + 3) / 4, nrt = (W + 3) / 4;
+        for (int id = tid; id < nct * nrt; id += NT) {
+            const int l0 = (id / nct) * 4, cb = (id % nct) * 4;
+            S acc[4][4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int jj = 0; jj < 4; ++jj) acc[i][jj] = S(0.0);
+            const S* mr = M + (size_t)l0 * LM + o;
+            for (int cc = 0; cc < wk; ++cc) {
+                S mv[4], vv[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) mv[i] = (l0 + i < W) ? mr[(size_t)i * LM + cc] : S(0.0);
+#pragma unroll
+                for (int jj = 0; jj < 4; ++jj) vv[jj] = Vs[(size_t)cc * LT + cb + jj];  // (cols >= wk: LT pad)
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int jj = 0; jj < 4; ++jj) acc[i][jj] = fma_s(mv[i], vv[jj], acc[i][jj]);
             }
-            M2[e] = v;
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int jj = 0; jj < 4; ++jj)
+                    if (l0 + i < W && cb + jj < wk) Tm[(size_t)(l0 + i) * LT + cb + jj] = acc[i][jj];
         }
         __syncthreads();
-        S* tmp = M;
-        M = M2;
-        M2 = tmp;
+        for (int e = tid; e < W * wk; e += NT) {
+            const int l = e / wk, c = e % wk;
+            M[(size_t)l * LM + o + c] = Tm[(size_t)l * LT + c];
+        }
+        __syncthreads();
     }
     for (int e = tid; e < a.WP * a.LDB; e += NT) {
         const int l = e / a.LDB, c = e % a.LDB;

@@ -372,7 +372,8 @@ int enqueue_groups(const Plan<S>& p, Workspace<S>& ws, cudaStream_t stream, bool
             NK(ncclGroupEnd());
         }
         if (qz && g >= NUV) CK(cudaStreamWaitEvent(stream, ws.ev_qz[bsel], 0));  // Q/Z of g-NUV done with U/V[bsel]
-        AccumArgs<S> aa{n, r, qp, j1, K, WP, LDB, ws.Qr, ws.Zr, ws.U[bsel], ws.V[bsel]};
+        AccumArgs<S> aa{n, r, qp, j1, K, WP, LDB, p.acc_bytes >= accum_smem_bytes<S>(r, q, true) ? 1 : 0, ws.Qr, ws.Zr,
+                        ws.U[bsel], ws.V[bsel]};
         if (root || qz) {
             accum_kernel<S, ACC_NT><<<dim3(K, 2), ACC_NT, p.acc_bytes, stream>>>(aa);
             CK(cudaGetLastError());
@@ -583,7 +584,8 @@ int run(int64_t n64, int64_t r64, S* H, int64_t ldh, S* T, int64_t ldt, S* Q, in
     const int strip_cap = (int)std::max<int64_t>(0, ((int64_t)chase_budget - (int64_t)chase_base) /
                                                         (int64_t)((r + 1) * sizeof(S)));
     const size_t chase_bytes = chase_smem_elems<S>(r, q, strip_cap) * sizeof(S);
-    const size_t acc_bytes = accum_smem_bytes<S>(r, q);
+    const bool acc_pre = accum_smem_bytes<S>(r, q, true) <= 200 * 1024;
+    const size_t acc_bytes = accum_smem_bytes<S>(r, q, acc_pre);
     const void* chase_fn = chase_kernel_for<S>(r);
     if (!chase_fn || q > 148) return HT_EUNSUPPORTED;  // one co-resident CTA per sweep
     const size_t ch_bytes = chain_bytes_rt<S>(WP, r, q, PM);
