@@ -70,7 +70,13 @@ constexpr int CH_LDX = CH_BM + 8;  // smem column stride of X (== 8 mod 16: conf
 __host__ __device__ constexpr int chain_ldb(int WP) { return WP + 8; }
 // warps along the window's columns: each warp owns WP/WN columns (a multiple of 8)
 __host__ __device__ constexpr int chain_wn(int WP) { return (WP % 64 == 0) ? 8 : 4; }
-__host__ __device__ constexpr int chain_nt(int WP) { return 32 * chain_wn(WP); }
+// warps along the tile rows: 8 warps per CTA (the chains are latency-bound; a warp's DMMA
+// sequence per step is what a step costs)
+#ifndef HT_CHAIN_WM
+#define HT_CHAIN_WM 2
+#endif
+__host__ __device__ constexpr int chain_wm(int WP) { return chain_wn(WP) == 8 ? 1 : HT_CHAIN_WM; }
+__host__ __device__ constexpr int chain_nt(int WP) { return 32 * chain_wn(WP) * chain_wm(WP); }
 
 // dynamic smem: [64 B mbarriers][circular X: (w+r) x CH_LDX][block ring][staircase refl.]
 template <typename S, int WP>
@@ -168,7 +174,8 @@ __device__ __forceinline__ bool chain_tile(const ChainParams<S>& P, int bid, uns
     constexpr int CH_NT = chain_nt(WP);
     constexpr int NW = CH_NT / 32;
     constexpr int WN = chain_wn(WP);
-    constexpr int MT = CH_BM / 8;    // 8-row tiles per warp (all CH_BM rows)
+    constexpr int WM = chain_wm(WP);
+    constexpr int MT = CH_BM / 8 / WM;  // 8-row tiles per warp
     constexpr int NTL = WP / (8 * WN);  // 8-col tiles per warp
     static_assert(WP % (8 * WN) == 0, "window padding");
     const int n = P.n, r = P.r, qp = P.qp, j1 = P.j1, K = P.K;
@@ -214,7 +221,7 @@ __device__ __forceinline__ bool chain_tile(const ChainParams<S>& P, int bid, uns
         if (kstart < 0) return false;
     }
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int wn = warp;
+    const int wn = warp % WN, wm = warp / WN;
     // ---- step sequence: from window khi downward, a step covers windows [klo, khi]: a whole
     // merge group [mg P, mg P + P - 1] when khi is its top and the tile is fully inside every
     // window of it (no staircase / column limit), else the single window khi ----
@@ -340,7 +347,7 @@ __device__ __forceinline__ bool chain_tile(const ChainParams<S>& P, int bid, uns
 #pragma unroll
             for (int nt = 0; nt < NTL; ++nt) acc_zero(acc[mt][nt]);
         const int nch = (wk + CH_KC - 1) / CH_KC;
-        const int rowb = lane >> 2;
+        const int rowb = wm * (CH_BM / WM) + (lane >> 2);
         const int colb = wn * (WP / WN) + (lane >> 2);
         for (int ch = 0; ch < nch; ++ch) {
             const int s = cseq % CH_STAGES;
