@@ -44,6 +44,23 @@ def _peaks():
         return {}
 
 
+def _dgemm_tflops(dev, n=8192, reps=3):
+    """cuBLAS DGEMM (torch.matmul, fp64, n^3) throughput on this GPU: the library reference for
+    the FP64 tensor ceiling next to the in-house DMMA probe; not on the path."""
+    import torch
+    a = torch.randn(n, n, dtype=torch.float64, device=dev)
+    b = torch.randn(n, n, dtype=torch.float64, device=dev)
+    torch.matmul(a, b)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        torch.matmul(a, b)
+    e1.record()
+    torch.cuda.synchronize()
+    return 2.0 * n ** 3 * reps / (e0.elapsed_time(e1) * 1e-3) / 1e12
+
+
 def _ncu_traffic(kernel, n, r, q):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel` from the committed
     `ncu --set full` capture summary (profiles/ncu_traffic.json), when it was taken on this
@@ -260,6 +277,7 @@ def main():
     # ---- roofline of the dominant kernel class (live CUDA-event durations) ----
     peaks = _peaks()
     dmma = ht.probe_dmma_tflops(20000)
+    dgemm = _dgemm_tflops(dev)
     fcnt_upd = (8.03 if not cplx else 8.03 * 4) * n ** 3  # counted update flops (H,T 4.03 + Q,Z 4.00) n^3
     # The dominant kernel class is the one with the largest share of the step's critical path:
     # the chase (K1) and the H/T chains run back to back on the caller's stream; the Q/Z chains
@@ -297,7 +315,7 @@ def main():
         "roofline_other": [x for x in (roof_k1, roof_ht, roof_qz) if x is not roof],
         "fraction_fp64_roofline": value / (world * dmma * 1e3),
         "gflops_counted": fcnt_upd / (ms_step * 1e-3) / 1e9,
-        "breakdown_ms": brk, "dmma_peak_tflops": dmma,
+        "breakdown_ms": brk, "dmma_peak_tflops": dmma, "cublas_dgemm_tflops": dgemm,
         "clocks": clk, "gpu_launches": launches,
         "measured_peaks": {k: peaks.get(k) for k in ("hbm_gbs", "bf16_tflops")},
     }
