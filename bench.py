@@ -44,6 +44,19 @@ def _peaks():
         return {}
 
 
+def _chase_latency(n, r, q, chase_ms, clk):
+    """K1 is a dependency chain: per group of qp sweeps the last sweep finishes after
+    K + 3(qp-1) sweep steps (lag 3).  Steps on the critical path of the call
+    and the measured cycles per such step (chase time incl. K2/K2m x SM clock / steps)."""
+    steps = 0
+    for j1 in range(1, n - 1, q):
+        qp = min(q, n - 1 - j1)
+        steps += 1 + (n - j1 - 2) // r + 3 * (qp - 1)
+    mhz = (clk or {}).get("sm_mhz") or 1965.0
+    return {"critical_path_steps": steps, "cycles_per_step": chase_ms * 1e-3 * mhz * 1e6 / max(steps, 1),
+            "sm_mhz": mhz}
+
+
 def _dgemm_tflops(dev, n=8192, reps=3):
     """cuBLAS DGEMM (torch.matmul, fp64, n^3) throughput on this GPU: the library reference for
     the FP64 tensor ceiling next to the in-house DMMA probe; not on the path."""
@@ -290,7 +303,8 @@ def main():
                "frac": ach_k1 / dfma, "traffic": _ncu_traffic("chase_kernel", n, r, q),
                "peak_source": "measured DFMA probe (ht_probe_dfma_tflops) on this GPU; MEASURED_PEAKS.json has no FP64 figure",
                "algorithmic": "RQ (2/3)r^2n^2 + generate band 2r(q+2)n^2 flops per call (a latency-bound chain)",
-               "share_of_step": brk["chase"] / ms_step}
+               "share_of_step": brk["chase"] / ms_step,
+               "latency_model": _chase_latency(n, r, q, brk["chase"], clk)}
     ht_cnt = (4.03 if not cplx else 4.03 * 4) * n ** 3  # counted H,T update flops (left + right) [V2]
     ach_ht = ht_cnt / (brk["ht_updates"] * 1e-3) / 1e12
     roof_ht = {"kernel": "chain_kernel, H/T right + left (K3/K4)", "bound": "tensor", "achieved": ach_ht, "peak": dmma,
