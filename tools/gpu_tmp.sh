@@ -1,5 +1,6 @@
 #!/bin/bash
 cd "$GRAFT_REPO_ROOT" || exit 1
-./exp/rqb > gpurun_out/rqb.txt 2>&1
-timeout 900 python -m pytest tests/test_gpu_parity.py -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_gpu.log
-K1ARGS="8192,64,32 8192,32,16,c" K1T="1" bash tools/gpu_k1abs.sh
+mkdir -p gpurun_out
+for i in 1 2 3 4; do
+    timeout 600 python bench.py --steps 3 --warmup 3 --no-cpu --no-e2e 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['ms_per_step'], round(d['breakdown_ms']['total'],1), d['clocks'])" >> gpurun_out/seq.log
+done
