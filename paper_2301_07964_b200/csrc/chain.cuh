@@ -46,6 +46,7 @@ struct ChainParams {
     const S* Zr;  // staircase reflectors: (qp*K) records of (r+1)
     int P;        // window merge factor (1 = off): steps cover P windows where the tile is fully inside
     int spread;   // > 0 (H/T, two jobs of equal tile count): block order longest chain first (see below)
+    long long* prof;  // optional (HT_K1PROF): cycles by phase of the longest tile's steps (8 slots)
 };
 
 // H/T chains are latency-bound by their longest tiles (right updates: the top row tiles walk
@@ -314,6 +315,18 @@ __device__ __forceinline__ bool chain_tile(const ChainParams<S>& P, int bid, uns
         cp_async_commit();
     }
     unsigned cseq = 0;  // consumer chunk sequence
+    // profile (tile 0 of job 0, thread 0): 0 wait+prefetch, 1 MMA, 2 epilogue, 3 staircase,
+    // 4 store, 5 steps, 6 merged steps, 7 staircase steps
+    const bool prf = P.prof && jb_ == 0 && bid == 0 && tid == 0;
+    long long pc_[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    long long tc_ = clock64();
+    auto tick = [&](int slot) {
+        if (prf) {
+            const long long now = clock64();
+            pc_[slot] += now - tc_;
+            tc_ = now;
+        }
+    };
     for (int k = kstart, klo = step_lo(kstart); k >= kend;) {
         const bool merged = klo < k;
         const int c0 = j1 + klo * r + 1;
@@ -339,6 +352,7 @@ __device__ __forceinline__ bool chain_tile(const ChainParams<S>& P, int bid, uns
                     cp_async_elem(&zsm[(size_t)t * (r + 1) + c], src + (size_t)t * K * (r + 1) + c);
         }
         cp_async_commit();
+        tick(0);
 
         // ---- Y = X(:, window) * B_k on the tensor cores ----
         Acc<S> acc[MT][NTL];
@@ -381,6 +395,7 @@ __device__ __forceinline__ bool chain_tile(const ChainParams<S>& P, int bid, uns
             ++cseq;
         }
         __syncthreads();  // all reads of X done
+        tick(1);
         // ---- epilogue: write Y back in place for the rows the mode updates ----
         const int ylo = (!merged && (mode == CM_A_LEFT || mode == CM_B_LEFT)) ? cstart(k) : 0;
         const int yhi = (!merged && mode == CM_AB_RIGHT) ? j1 + max(0, (k - qp + 1) * r) : 0x7fffffff;
@@ -401,6 +416,7 @@ __device__ __forceinline__ bool chain_tile(const ChainParams<S>& P, int bid, uns
                     }
                 }
         }
+        tick(2);
         if (stair) {  // Alg. 4 lines 4-9: rows i5s..i4(k,j) get Z_k^j one by one, j ascending
             cp_async_wait_all();
             __syncthreads();
@@ -440,11 +456,18 @@ __device__ __forceinline__ bool chain_tile(const ChainParams<S>& P, int bid, uns
             }
         }
         __syncthreads();
+        tick(3);
         // columns [cn, wk) are final for this group; [0, cn) stay as window k-1's carry
         {
             int po = p + cn;
             if (po >= CIRC) po -= CIRC;
             store_cols(c0 + cn, wk - cn, po);
+        }
+        tick(4);
+        if (prf) {
+            pc_[5] += 1;
+            pc_[6] += merged;
+            pc_[7] += stair;
         }
         p -= shift;
         if (p < 0) p += CIRC;
@@ -452,6 +475,8 @@ __device__ __forceinline__ bool chain_tile(const ChainParams<S>& P, int bid, uns
         klo = nklo;
     }
     cp_async_wait_all();
+    if (prf)
+        for (int i = 0; i < 8; ++i) atomicAdd((unsigned long long*)&P.prof[i], (unsigned long long)pc_[i]);
     return true;
 }
 

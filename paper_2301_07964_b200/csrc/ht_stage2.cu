@@ -190,7 +190,7 @@ struct Workspace {
     S *U[NUV] = {}, *V[NUV] = {}, *MU[NUV] = {}, *MV[NUV] = {}, *Zr = nullptr, *Qr = nullptr, *Tr = nullptr, *Mg = nullptr;
     int* prog = nullptr;
     long long* k1prof = nullptr;
-    long long k1prof_host[16] = {0};
+    long long k1prof_host[32] = {0};  // [0,16) K1, [16,24) right chains, [24,32) left chains
     cudaStream_t side = nullptr;
     cudaEvent_t ev_uv[NUV] = {}, ev_qz[NUV] = {};
     bool async = true;
@@ -218,8 +218,8 @@ struct Workspace {
         if (chase_dense_catchup<S>(p.r)) CK(mal((void**)&Mg, (size_t)p.Kmax * mcatch_st(p.q, p.r) * sizeof(S)));
         CK(mal((void**)&prog, (size_t)(5 * p.q + 2) * sizeof(int)));
         if (k1p) {
-            CK(mal((void**)&k1prof, 16 * sizeof(long long)));
-            CK(cudaMemsetAsync(k1prof, 0, 16 * sizeof(long long), stream));
+            CK(mal((void**)&k1prof, 32 * sizeof(long long)));
+            CK(cudaMemsetAsync(k1prof, 0, 32 * sizeof(long long), stream));
         }
         if (p.qz()) {
             int lo = 0, hi = 0;
@@ -278,6 +278,13 @@ void print_k1prof(const long long* h) {
     for (int i = 0; i < 16; ++i)
         if (i != 11 && h[i]) fprintf(stderr, " %s=%.0f", nm[i], h[i] / steps);
     fprintf(stderr, " all=%.0f\n", tot / steps);
+    for (int c = 0; c < 2; ++c) {  // apply chains: the longest tile (tile 0 of H)
+        const long long* g = h + 16 + 8 * c;
+        const double st = g[5] > 0 ? (double)g[5] : 1.0;
+        fprintf(stderr, "%s chain, tile 0 of H, cycles per step: wait+prefetch=%.0f mma=%.0f epilogue=%.0f "
+                        "staircase=%.0f store=%.0f (steps %lld, merged %lld, with staircase %lld)\n",
+                c == 0 ? "right" : "left", g[0] / st, g[1] / st, g[2] / st, g[3] / st, g[4] / st, g[5], g[6], g[7]);
+    }
 }
 
 // Enqueue every group of the reduction: chase (K1) -> accumulate U/V (K2) -> H/T right and left
@@ -392,11 +399,11 @@ int enqueue_groups(const Plan<S>& p, Workspace<S>& ws, cudaStream_t stream, bool
         if (root) {
             ChainParams<S> pr{n, r, qp, j1, K, {{p.H, p.ldh, ws.V[bsel], ws.MV[bsel], CM_AB_RIGHT, 0, tiles, 0},
                                                 {p.T, p.ldt, ws.V[bsel], ws.MV[bsel], CM_AB_RIGHT, 0, tiles, 0}}, 2, ws.Zr, p.P,
-                              chain_spread(p.nsm)};
+                              chain_spread(p.nsm), ws.k1prof ? ws.k1prof + 16 : nullptr};
             if (int rc = chain<S>(pr, WP, 2 * tiles, r, q, stream)) return rc;
             ChainParams<S> pl{n, r, qp, j1, K, {{p.H, p.ldh, ws.U[bsel], ws.MU[bsel], CM_A_LEFT, 1, tiles, 0},
                                                 {p.T, p.ldt, ws.U[bsel], ws.MU[bsel], CM_B_LEFT, 1, tiles, 0}}, 2, ws.Zr, p.P,
-                              chain_spread(p.nsm)};
+                              chain_spread(p.nsm), ws.k1prof ? ws.k1prof + 24 : nullptr};
             if (int rc = chain<S>(pl, WP, 2 * tiles, r, q, stream)) return rc;
             g_last_launches += 2;
         }
