@@ -1,5 +1,7 @@
 #!/bin/bash
 cd "$GRAFT_REPO_ROOT" || exit 1
-timeout 300 python tools/k1prof.py 8192 64 32 > gpurun_out/ncu_pre64.log 2>&1 || exit 1
-HT_NO_GRAPH=1 timeout 900 ncu --set full --clock-control none --import-source on -k regex:chase_kernel --launch-skip 60 --launch-count 1 \
-  -f -o gpurun_out/prof_chase64 python tools/k1prof.py 8192 64 32 > gpurun_out/ncu_chase64.log 2>&1
+rm -f gpurun_out/chp.log
+for tl in 74 100; do
+  echo "== WY tile $tl" >> gpurun_out/chp.log
+  HT_CHAIN_PROF_TILE=$tl HT_K1PROF=1 HT_K1PROF_T=0 timeout 300 python tools/k1prof.py 4096 16 32 2>&1 | grep -E "right chain," | tail -1 >> gpurun_out/chp.log
+done
