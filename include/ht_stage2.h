@@ -17,9 +17,13 @@
  * All matrix pointers are DEVICE pointers on the calling thread's current
  * CUDA device (cudaSetDevice before the call).
  *
- * Ownership: the caller owns all buffers; the update is in place.  Workspace
- * is allocated stream-ordered on `stream` (cudaMallocAsync) and freed before
- * return; no pointer is retained after return.
+ * Ownership: the caller owns all buffers; the update is in place.  The default
+ * path replays a CUDA graph of the whole reduction that the library caches per
+ * host thread, keyed by (device, n, r, q, buffer pointers and leading
+ * dimensions); each cached graph owns its workspace (plain cudaMalloc, at most 4
+ * entries, the oldest evicted).  Profiling and multi-GPU calls allocate
+ * workspace stream-ordered on `stream` and free it before return.  No caller
+ * pointer is dereferenced after the work enqueued by the call completes.
  *
  * Streams: stream-ordered on `stream` (like cuSOLVER).  Internal streams are
  * joined back to `stream` with events.  The host blocks once at entry (input
@@ -67,7 +71,7 @@ extern "C" {
 
 /* Tunables (NULL = defaults).  q: sweeps per group ("q");
  * 0 = default (environment HT_Q, else a per-r choice documented in DESIGN.md).
- * chase_ctas: CTAs of the wavefront chase kernel (0 = min(q, 32)).
+ * chase_ctas: reserved (the chase runs one CTA per sweep plus far-strip helpers).
  * root: result rank for comm != NULL.  flags: bit 0 = skip input validation,
  * bit 1 = record per-kernel-class device times (see ht_last_timing). */
 typedef struct ht_opts {
