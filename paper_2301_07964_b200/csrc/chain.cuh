@@ -18,6 +18,8 @@
 // staircase (rows i5s..i4(k,j), reflector by reflector, Alg. 4 lines 4-9) and untouched
 // rows; left updates touch columns > i5 (H) / > i6 (T) only.
 #pragma once
+#include <type_traits>
+
 #include "scalar.cuh"
 
 #ifndef IDX
@@ -46,7 +48,8 @@ struct ChainParams {
     const S* Zr;  // staircase reflectors: (qp*K) records of (r+1)
     int P;        // window merge factor (1 = off): steps cover P windows where the tile is fully inside
     int spread;   // > 0 (H/T, two jobs of equal tile count): block order longest chain first (see below)
-    long long* prof;  // optional (HT_K1PROF): cycles by phase of the longest tile's steps (8 slots)
+    long long* prof;  // optional (HT_K1PROF): cycles by phase of one tile's steps (8 slots)
+    int prof_tile;    // the profiled tile of job 0 (HT_CHAIN_PROF_TILE)
 };
 
 // H/T chains are latency-bound by their longest tiles (right updates: the top row tiles walk
@@ -67,6 +70,10 @@ constexpr int CH_BM = 32;      // tile rows per CTA (one warp row of 4 m8 tiles)
 constexpr int CH_KC = 16;      // k rows per ring chunk
 constexpr int CH_STAGES = 3;   // ring depth
 constexpr int CH_LDX = CH_BM + 8;  // smem column stride of X (== 8 mod 16: conflict-free)
+#ifndef HT_STAIR_BZ
+#define HT_STAIR_BZ 4
+#endif
+constexpr int CH_SBZ = HT_STAIR_BZ;  // staircase reflectors per compact-WY block
 
 __host__ __device__ constexpr int chain_ldb(int WP) { return WP + 8; }
 // warps along the window's columns: each warp owns WP/WN columns (a multiple of 8)
@@ -83,7 +90,8 @@ __host__ __device__ constexpr int chain_nt(int WP) { return 32 * chain_wn(WP) * 
 template <typename S, int WP>
 __host__ __device__ constexpr size_t chain_smem_bytes(int r, int q, int P = 1) {
     return 64 + (size_t)(P > 1 ? q + 2 * P * r - 1 : q + r - 1 + r) * CH_LDX * sizeof(S) +
-           (size_t)CH_STAGES * CH_KC * chain_ldb(WP) * sizeof(S) + (size_t)(q + 1) * (r + 1) * sizeof(S);
+           (size_t)CH_STAGES * CH_KC * chain_ldb(WP) * sizeof(S) + (size_t)(q + 1) * (r + 1) * sizeof(S) +
+           (size_t)2 * ((q + CH_SBZ - 1) / CH_SBZ) * CH_SBZ * CH_SBZ * sizeof(S);  // staircase block factors
 }
 
 // ---- PTX helpers ---------------------------------------------------------------------
@@ -317,7 +325,7 @@ __device__ __forceinline__ bool chain_tile(const ChainParams<S>& P, int bid, uns
     unsigned cseq = 0;  // consumer chunk sequence
     // profile (tile 0 of job 0, thread 0): 0 wait+prefetch, 1 MMA, 2 epilogue, 3 staircase,
     // 4 store, 5 steps, 6 merged steps, 7 staircase steps
-    const bool prf = P.prof && jb_ == 0 && bid == 0 && tid == 0;
+    const bool prf = P.prof && jb_ == 0 && bid == P.prof_tile && tid == 0;
     long long pc_[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     long long tc_ = clock64();
     auto tick = [&](int slot) {
@@ -417,43 +425,132 @@ __device__ __forceinline__ bool chain_tile(const ChainParams<S>& P, int bid, uns
                 }
         }
         tick(2);
-        if (stair) {  // Alg. 4 lines 4-9: rows i5s..i4(k,j) get Z_k^j one by one, j ascending
+        if (stair) {
+            // Alg. 4 lines 4-9: rows i5s..i4(k,j) get Z_k^j, j ascending, in blocks of BZ reflectors
+            // (compact WY per block: Z_t ... Z_{t+BZ-1} = I - Y T Y^*): the BZ dots of a row are
+            // independent, so a block costs about one reflector's latency.  A row gets the
+            // reflectors t with g <= i4a(t) (a suffix); zeroing the dots outside it and the upper
+            // triangular T keep exactly that suffix.  Steps without a reflector have a zero record.
             cp_async_wait_all();
             __syncthreads();
-            const int row = tid >> 2, part = tid & 3;  // 4 threads per row (CH_NT/4 >= CH_BM)
+            tick(2);  // (profile: the wait for the staircase data counts as epilogue)
+            constexpr int TPR = CH_NT / CH_BM, BZ = CH_SBZ;  // threads per row, reflectors per block
+            const int row = tid / TPR, part = tid % TPR;
             const int g = R0 + row;
             const bool active = row < nr && g >= i5s && g <= rowmax(k);
-            // reflector t reaches rows <= i4a(t) = j1 + max(0,(k+t-qp+1)r): start at the first t
-            // reaching this tile's staircase rows (uniform); steps without a reflector have a zero
-            // record (sigma = 0)
             const int lo = max(i5s, R0);
-            int t0 = 1;
+            int t0 = 1;  // first reflector reaching this tile's staircase rows (uniform)
             if (j1 < lo) t0 = max(1, (lo - j1 + r - 1) / r - k + qp - 1);
-            for (int t = t0; t < qp; ++t) {
-                const int m = min(r, n - (j1 + t + k * r));
-                if (m < 2) continue;
-                const int i4a = j1 + max(0, (k + t - qp + 1) * r);
-                const S* zr = zsm + (size_t)t * (r + 1);
-                const S sig = zr[r];
-                if (is_zero(sig)) continue;
-                S sdot = S(0.0);
-                if (active && g <= i4a)
-                    for (int c = part; c < m; c += 4) {
-                        int pos = p + t + c;
-                        if (pos >= CIRC) pos -= CIRC;
-                        sdot = fma_s(X[pos * CH_LDX + row], zr[c], sdot);
+            const int nbk = (qp - t0 + BZ - 1) / BZ;
+            S* Gs = zsm + (size_t)(qp + 1) * (r + 1);
+            S* Ts = Gs + (size_t)((qp + BZ - 1) / BZ) * BZ * BZ;
+            auto msz = [&](int t) { return (t < qp) ? min(r, n - (j1 + t + k * r)) : 0; };
+            auto zrec = [&](int t) { return zsm + (size_t)t * (r + 1); };
+            // G(i,j) = z_i^* z_j over the columns both touch (i < j within a block)
+            for (int e = tid; e < nbk * BZ * BZ; e += CH_NT) {
+                const int bi = e / (BZ * BZ), i = (e / BZ) % BZ, jj = e % BZ;
+                const int ti = t0 + bi * BZ + i, tj = t0 + bi * BZ + jj;
+                S gg = S(0.0);
+                if (i < jj && tj < qp) {
+                    const int mi = msz(ti), mj = msz(tj);
+                    const S* zi = zrec(ti);
+                    const S* zj = zrec(tj);
+                    for (int c = tj; c < min(ti + mi, tj + mj); ++c) gg += conj_mul(zi[c - ti], zj[c - tj]);
+                }
+                Gs[e] = gg;
+            }
+            __syncthreads();
+            // block factor (xLARFT forward): T(i,i) = sigma_i, T(i,j) = -sigma_j sum_l T(i,l) G(l,j)
+            // rows of T are independent given G: T(i,j) = -sigma_j sum_{l=i}^{j-1} T(i,l) G(l,j),
+            // so one thread per (block, row) runs along its row
+            for (int e = tid; e < nbk * BZ; e += CH_NT) {
+                const int bi = e / BZ, i = e % BZ;
+                S* Tr = Ts + ((size_t)bi * BZ + i) * BZ;
+                const S* Gb = Gs + (size_t)bi * BZ * BZ;
+                S tr[BZ];
+#pragma unroll
+                for (int jj = 0; jj < BZ; ++jj) {
+                    const int tj = t0 + bi * BZ + jj;
+                    const S sj = (tj < qp && msz(tj) >= 2) ? zrec(tj)[r] : S(0.0);
+                    S v = S(0.0);
+                    if (jj == i) {
+                        v = sj;
+                    } else if (jj > i) {
+                        S acc = S(0.0);
+#pragma unroll
+                        for (int l = 0; l < BZ; ++l)
+                            if (l >= i && l < jj) acc += tr[l] * Gb[l * BZ + jj];
+                        v = -(sj * acc);
                     }
-                sdot += shfl_xor(sdot, 1);
-                sdot += shfl_xor(sdot, 2);
-                if (active && g <= i4a) {
-                    sdot = sdot * sig;
-                    for (int c = part; c < m; c += 4) {
-                        int pos = p + t + c;
-                        if (pos >= CIRC) pos -= CIRC;
-                        X[pos * CH_LDX + row] -= sdot * conjv(zr[c]);
-                    }
+                    tr[jj] = v;
+                    Tr[jj] = v;
                 }
             }
+            __syncthreads();
+            tick(0);  // (profile: the block factors count as wait+prefetch)
+            // block rounds, with compile-time trip counts (MR >= r): no loop branches in the chain
+            auto rounds = [&](auto mrc) {
+                constexpr int MR = decltype(mrc)::value;
+                constexpr int ND = (MR + TPR - 1) / TPR, NU = (BZ - 1 + MR + TPR - 1) / TPR;
+                for (int bi = 0; bi < nbk; ++bi) {
+                    const int tb = t0 + bi * BZ;
+                    S wv[BZ];
+                    int mt[BZ];
+#pragma unroll
+                    for (int i = 0; i < BZ; ++i) {
+                        const int t = tb + i;
+                        const int m = msz(t);
+                        mt[i] = m;
+                        const bool on = active && m >= 2 && g <= j1 + max(0, (k + t - qp + 1) * r);
+                        const S* zr = zrec(t);
+                        S d = S(0.0);
+#pragma unroll
+                        for (int u = 0; u < ND; ++u) {
+                            const int c = part + u * TPR;
+                            if (on && c < m) {
+                                int pos = p + t + c;
+                                if (pos >= CIRC) pos -= CIRC;
+                                d = fma_s(X[pos * CH_LDX + row], zr[c], d);
+                            }
+                        }
+                        wv[i] = d;
+                    }
+#pragma unroll
+                    for (int o = 1; o < TPR; o <<= 1)
+#pragma unroll
+                        for (int i = 0; i < BZ; ++i) wv[i] += shfl_xor(wv[i], o);
+                    S w2[BZ];
+#pragma unroll
+                    for (int i = 0; i < BZ; ++i) {
+                        S acc = S(0.0);
+#pragma unroll
+                        for (int jj = 0; jj <= i; ++jj) acc += wv[jj] * Ts[(bi * BZ + jj) * BZ + i];
+                        w2[i] = acc;
+                    }
+                    if (active) {
+#pragma unroll
+                        for (int u = 0; u < NU; ++u) {  // window columns tb + cc
+                            const int cc = part + u * TPR;
+                            S acc = S(0.0);
+#pragma unroll
+                            for (int i = 0; i < BZ; ++i) {
+                                const int ci = cc - i;
+                                if (ci >= 0 && ci < mt[i]) acc += w2[i] * conjv(zrec(tb + i)[ci]);
+                            }
+                            if (cc < BZ - 1 + mt[0] && tb + cc < wk) {
+                                int pos = p + tb + cc;
+                                if (pos >= CIRC) pos -= CIRC;
+                                X[pos * CH_LDX + row] -= acc;
+                            }
+                        }
+                    }
+                }
+            };
+            if (r <= 8) rounds(std::integral_constant<int, 8>{});
+            else if (r <= 16) rounds(std::integral_constant<int, 16>{});
+            else if (r <= 32) rounds(std::integral_constant<int, 32>{});
+            else if (r <= 64) rounds(std::integral_constant<int, 64>{});
+            else rounds(std::integral_constant<int, 128>{});
         }
         __syncthreads();
         tick(3);

@@ -281,7 +281,7 @@ void print_k1prof(const long long* h) {
     for (int c = 0; c < 2; ++c) {  // apply chains: the longest tile (tile 0 of H)
         const long long* g = h + 16 + 8 * c;
         const double st = g[5] > 0 ? (double)g[5] : 1.0;
-        fprintf(stderr, "%s chain, tile 0 of H, cycles per step: wait+prefetch=%.0f mma=%.0f epilogue=%.0f "
+        fprintf(stderr, "%s chain, profiled tile of H (HT_CHAIN_PROF_TILE), cycles per step: wait+prefetch=%.0f mma=%.0f epilogue=%.0f "
                         "staircase=%.0f store=%.0f (steps %lld, merged %lld, with staircase %lld)\n",
                 c == 0 ? "right" : "left", g[0] / st, g[1] / st, g[2] / st, g[3] / st, g[4] / st, g[5], g[6], g[7]);
     }
@@ -399,11 +399,13 @@ int enqueue_groups(const Plan<S>& p, Workspace<S>& ws, cudaStream_t stream, bool
         if (root) {
             ChainParams<S> pr{n, r, qp, j1, K, {{p.H, p.ldh, ws.V[bsel], ws.MV[bsel], CM_AB_RIGHT, 0, tiles, 0},
                                                 {p.T, p.ldt, ws.V[bsel], ws.MV[bsel], CM_AB_RIGHT, 0, tiles, 0}}, 2, ws.Zr, p.P,
-                              chain_spread(p.nsm), ws.k1prof ? ws.k1prof + 16 : nullptr};
+                              chain_spread(p.nsm), ws.k1prof ? ws.k1prof + 16 : nullptr,
+                              getenv("HT_CHAIN_PROF_TILE") ? atoi(getenv("HT_CHAIN_PROF_TILE")) : 0};
             if (int rc = chain<S>(pr, WP, 2 * tiles, r, q, stream)) return rc;
             ChainParams<S> pl{n, r, qp, j1, K, {{p.H, p.ldh, ws.U[bsel], ws.MU[bsel], CM_A_LEFT, 1, tiles, 0},
                                                 {p.T, p.ldt, ws.U[bsel], ws.MU[bsel], CM_B_LEFT, 1, tiles, 0}}, 2, ws.Zr, p.P,
-                              chain_spread(p.nsm), ws.k1prof ? ws.k1prof + 24 : nullptr};
+                              chain_spread(p.nsm), ws.k1prof ? ws.k1prof + 24 : nullptr,
+                              getenv("HT_CHAIN_PROF_TILE") ? atoi(getenv("HT_CHAIN_PROF_TILE")) : 0};
             if (int rc = chain<S>(pl, WP, 2 * tiles, r, q, stream)) return rc;
             g_last_launches += 2;
         }
