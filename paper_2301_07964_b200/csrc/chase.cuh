@@ -810,19 +810,21 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
         }
         k1_commit();
         K1_TICK(1);
-        // the strip is only needed after the RQ: its own (newest) group, waited for there
-        if (jb <= n && nx > 0) {
-            if (gen) {
-                for (int cc = warp; cc < m; cc += NW) {
-                    for (int rr = lane; rr < stA; rr += 32) k1_ld(&strip[rr * SLD + cc], &IDX(a.A, a.lda, i4 + rr, i1 + cc));
-                    for (int rr = lane; rr < stB; rr += 32)
-                        k1_ld(&strip[(stA + rr) * SLD + cc], &IDX(a.B, a.ldb, i4 + rr, i1 + cc));
-                }
+        // the strip is only needed after the RQ: its own (newest) group, waited for there.  On the
+        // dense path its loads are issued by warps 2.. during the fused catch-up (S2+S3) instead
+        auto issue_strip = [&](int w0) {
+            for (int cc = warp - w0; cc < m; cc += NW - w0) {
+                for (int rr = lane; rr < stA; rr += 32) k1_ld(&strip[rr * SLD + cc], &IDX(a.A, a.lda, i4 + rr, i1 + cc));
+                for (int rr = lane; rr < stB; rr += 32)
+                    k1_ld(&strip[(stA + rr) * SLD + cc], &IDX(a.B, a.ldb, i4 + rr, i1 + cc));
             }
-        }
-        k1_commit();
+        };
+        const bool late_strip = MK && gen;
+        if (jb <= n && nx > 0 && gen && !late_strip) issue_strip(0);
+        if (!late_strip) k1_commit();
         K1_TICK(10);
-        k1_wait_group<1>();
+        if (late_strip) k1_wait_group<0>();
+        else k1_wait_group<1>();
         __syncthreads();
         K1_TICK(1);
         if (jb <= n && nx > 0) {
@@ -956,7 +958,9 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
                         }
                         if (hasB && !cu)
                             for (int i = tid - 32; i < m; i += NT - 32) Cb[i + (m - 1) * LDC] = ys[t + i];
+                        if (warp >= 2) issue_strip(2);
                     }
+                    k1_commit();  // the strip group (empty for warps 0, 1)
                     __syncthreads();
                     K1_TICK(7);
                     tau = scal[0];

@@ -6,7 +6,7 @@ rm -f gpurun_out/k1abs.log
 for a in $K1ARGS; do
   for tt in $K1T; do
     echo "== $a t0=$tt" >> gpurun_out/k1abs.log
-    HT_K1PROF=1 HT_K1PROF_T=$tt timeout 300 python tools/k1prof.py ${a//,/ } 2>&1 | tail -3 >> gpurun_out/k1abs.log
+    HT_K1PROF=1 HT_K1PROF_T=$tt timeout 300 python tools/k1prof.py ${a//,/ } 2>&1 | grep -E "K1 cycles|wall" >> gpurun_out/k1abs.log
   done
 done
 echo done
