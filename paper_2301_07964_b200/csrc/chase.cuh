@@ -819,7 +819,8 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
                     k1_ld(&strip[(stA + rr) * SLD + cc], &IDX(a.B, a.ldb, i4 + rr, i1 + cc));
             }
         };
-        const bool late_strip = MK && gen;
+        // (dense path: during the fused catch-up + left reflector; WY path: during the catch-up)
+        const bool late_strip = gen && (MK || cu);
         if (jb <= n && nx > 0 && gen && !late_strip) issue_strip(0);
         if (!late_strip) k1_commit();
         K1_TICK(10);
@@ -892,7 +893,10 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
                         }
                         xv[i] -= acc;
                     }
+                } else if (late_strip && warp >= 2) {
+                    issue_strip(2);  // (the warps the WY catch-up leaves idle)
                 }
+                if (late_strip) k1_commit();  // the strip group (empty for warps 0, 1)
                 __syncthreads();
                 if (hasB && gen)
                     for (int i = tid; i < m; i += NT)
