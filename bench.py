@@ -91,8 +91,9 @@ def _ncu_traffic(kernel, n, r, q):
 
 class ClockSampler:
     """SM clocks + throttle reasons DURING the timed region (B200_PROFILING.md), sampled every
-    250 ms in-process through NVML (lighter than an nvidia-smi process, whose polling was seen to
-    stall the host side of the timed loop now and then); nvidia-smi is the fallback."""
+    500 ms in-process through NVML (two queries per sample; lighter than an nvidia-smi process,
+    whose polling was seen to stall the host side of the timed loop now and then); nvidia-smi is
+    the fallback."""
 
     Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
@@ -131,15 +132,17 @@ class ClockSampler:
 
     def _poll(self):
         nv = self.nvml
-        while not self.stop_ev.is_set():
+        try:
+            mx = float(nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM))
+        except Exception:
+            mx = 0.0
+        while not self.stop_ev.wait(0.5):
             try:
                 sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
-                mx = nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)
                 rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
-                self.samples.append((float(sm), float(mx), int(rs)))
+                self.samples.append((float(sm), mx, int(rs)))
             except Exception:
                 pass
-            self.stop_ev.wait(0.25)
 
     def _read(self):
         for line in self.proc.stdout:
@@ -150,6 +153,13 @@ class ClockSampler:
             self.stop_ev.set()
             self.th.join(timeout=5)
             nv = self.nvml
+            if not self.samples:  # a timed region shorter than one period: sample at its end
+                try:
+                    self.samples.append((float(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)),
+                                         float(nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)),
+                                         int(nv.nvmlDeviceGetCurrentClocksEventReasons(self.h))))
+                except Exception:
+                    pass
             bits = {"hw_slowdown": nv.nvmlClocksEventReasonHwSlowdown,
                     "hw_thermal_slowdown": nv.nvmlClocksEventReasonHwThermalSlowdown,
                     "sw_thermal_slowdown": nv.nvmlClocksEventReasonSwThermalSlowdown,
@@ -311,7 +321,6 @@ def main():
     barrier()
     torch.cuda.synchronize()
     clocks.start()
-    time.sleep(0.3)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
     for _ in range(args.steps):

@@ -1,9 +1,11 @@
 #!/bin/bash
 cd "$GRAFT_REPO_ROOT" || exit 1
-timeout 900 python -m pytest tests/test_gpu_parity.py -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_gpu.log
-rm -f gpurun_out/chp.log
-for tl in 74; do
-  echo "== tile $tl" >> gpurun_out/chp.log
-  HT_CHAIN_PROF_TILE=$tl HT_K1PROF=1 HT_K1PROF_T=0 timeout 300 python tools/k1prof.py 4096 16 32 2>&1 | grep -E "right chain," | tail -1 >> gpurun_out/chp.log
+rm -f gpurun_out/seq.log
+for i in 1 2; do
+  for smi in 0 1; do
+    if [ $smi = 1 ]; then export HT_NO_SMI=1; else unset HT_NO_SMI; fi
+    for c in 1 2; do
+      timeout 600 python bench.py --config $c --steps 10 --warmup 3 --no-cpu --no-e2e 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('cfg$c nosmi=$smi', round(d['ms_per_step'],2), round(d['breakdown_ms']['total'],1), d['clocks'].get('samples'))" >> gpurun_out/seq.log
+    done
+  done
 done
-HTARGS="4096,16,32 8192,64,32 8192,32,32,c" bash tools/gpu_ht.sh
