@@ -90,10 +90,14 @@ def _ncu_traffic(kernel, n, r, q):
 
 
 class ClockSampler:
-    """SM clocks + throttle reasons DURING the timed region (B200_PROFILING.md), sampled every
-    500 ms in-process through NVML (two queries per sample; lighter than an nvidia-smi process,
-    whose polling was seen to stall the host side of the timed loop now and then); nvidia-smi is
-    the fallback."""
+    """SM clocks and throttling DURING the timed region (B200_PROFILING.md), through NVML
+    in-process with as few driver queries as possible (frequent NVML / nvidia-smi polling was
+    measured to stall the host side of the timed loop now and then, +10-20 % on a step):
+    - the power and thermal violation-time counters (cumulative, ns) before and after the region:
+      any increase means the region was throttled (reported as sw_power_cap / *_thermal_slowdown);
+    - the SM clock and the current event-reason bits sampled once 100 ms into the region and once
+      at its end.
+    nvidia-smi is the fallback when NVML is unavailable."""
 
     Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
@@ -108,6 +112,24 @@ class ClockSampler:
         self.samples = []  # (sm_mhz, max_mhz, reason bits)
         self.stop_ev = threading.Event()
 
+    def _violations(self):
+        nv = self.nvml
+        out = {}
+        for nm, pol in (("power", nv.NVML_PERF_POLICY_POWER), ("thermal", nv.NVML_PERF_POLICY_THERMAL)):
+            try:
+                out[nm] = int(nv.nvmlDeviceGetViolationStatus(self.h, pol).violationTime)
+            except Exception:
+                pass
+        return out
+
+    def _sample(self):
+        nv = self.nvml
+        try:
+            self.samples.append((float(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)), self.mx,
+                                 int(nv.nvmlDeviceGetCurrentClocksEventReasons(self.h))))
+        except Exception:
+            pass
+
     def start(self):
         if os.environ.get("HT_NO_SMI"):
             return
@@ -116,6 +138,11 @@ class ClockSampler:
             pynvml.nvmlInit()
             self.nvml = pynvml
             self.h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            try:
+                self.mx = float(pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM))
+            except Exception:
+                self.mx = 0.0
+            self.v0 = self._violations()
             self.th = threading.Thread(target=self._poll, daemon=True)
             self.th.start()
             return
@@ -131,18 +158,8 @@ class ClockSampler:
             self.proc = None
 
     def _poll(self):
-        nv = self.nvml
-        try:
-            mx = float(nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM))
-        except Exception:
-            mx = 0.0
-        while not self.stop_ev.wait(0.5):
-            try:
-                sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
-                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
-                self.samples.append((float(sm), mx, int(rs)))
-            except Exception:
-                pass
+        if not self.stop_ev.wait(0.1):
+            self._sample()
 
     def _read(self):
         for line in self.proc.stdout:
@@ -153,26 +170,24 @@ class ClockSampler:
             self.stop_ev.set()
             self.th.join(timeout=5)
             nv = self.nvml
-            if not self.samples:  # a timed region shorter than one period: sample at its end
-                try:
-                    self.samples.append((float(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)),
-                                         float(nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)),
-                                         int(nv.nvmlDeviceGetCurrentClocksEventReasons(self.h))))
-                except Exception:
-                    pass
+            self._sample()
+            v1 = self._violations()
             bits = {"hw_slowdown": nv.nvmlClocksEventReasonHwSlowdown,
                     "hw_thermal_slowdown": nv.nvmlClocksEventReasonHwThermalSlowdown,
                     "sw_thermal_slowdown": nv.nvmlClocksEventReasonSwThermalSlowdown,
                     "sw_power_cap": nv.nvmlClocksEventReasonSwPowerCap}
             reasons = {nm for _, _, rs in self.samples for nm, b in bits.items() if rs & b}
+            if v1.get("power", 0) > self.v0.get("power", 0):
+                reasons.add("sw_power_cap")
+            if v1.get("thermal", 0) > self.v0.get("thermal", 0):
+                reasons.add("sw_thermal_slowdown")
             sm = [x[0] for x in self.samples]
-            mx = [x[1] for x in self.samples]
             try:
                 nv.nvmlShutdown()
             except Exception:
                 pass
-            return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                    "reasons": sorted(reasons), "samples": len(sm), "source": "nvml"}
+            return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": self.mx or None,
+                    "reasons": sorted(reasons), "samples": len(sm), "source": "nvml (+ violation counters)"}
         if not self.proc:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["clock sampling unavailable"]}
         self.proc.terminate()
