@@ -168,11 +168,12 @@ struct Plan {
     int helpers = 1;  // far-strip helper CTAs per sweep in the chase
     int P = 1;        // window merge factor of the apply chains (K2m)
     int nsm = 148;    // SMs (longest-chain-first tile order of the H/T chains)
+    bool qz_late = false;  // Q/Z chains of a group start after its H/T chains (HT_QZ_LATE)
     size_t mrg_bytes = 0;
     bool is_root() const { return comm == nullptr || rank == root; }
     bool qz() const { return Q || Z; }
     bool same(const Plan& o) const {
-        return n == o.n && r == o.r && q == o.q && strip_cap == o.strip_cap && helpers == o.helpers && P == o.P && H == o.H && ldh == o.ldh &&
+        return n == o.n && r == o.r && q == o.q && strip_cap == o.strip_cap && helpers == o.helpers && P == o.P && qz_late == o.qz_late && H == o.H && ldh == o.ldh &&
                T == o.T && ldt == o.ldt && Q == o.Q && ldq == o.ldq && Z == o.Z && ldz == o.ldz;
     }
 };
@@ -392,7 +393,9 @@ int enqueue_groups(const Plan<S>& p, Workspace<S>& ws, cudaStream_t stream, bool
                 ++g_last_launches;
             }
         }
-        if (qz) CK(cudaEventRecord(ws.ev_uv[bsel], stream));
+        // Q/Z chains of group g start after K2 (their blocks), or -- p.qz_late -- after the group's
+        // H/T chains, so that those (on the critical path) do not share SMs with them
+        if (qz && !p.qz_late) CK(cudaEventRecord(ws.ev_uv[bsel], stream));
         if (prof) CK(cudaEventRecord(ev[5 * g + 1], stream));
         // ---- apply phase: right updates of H, T (staircase + V_k), then left (U_k^*) ----
         const int tiles = (n + CH_BM - 1) / CH_BM;
@@ -409,6 +412,7 @@ int enqueue_groups(const Plan<S>& p, Workspace<S>& ws, cudaStream_t stream, bool
             if (int rc = chain<S>(pl, WP, 2 * tiles, r, q, stream)) return rc;
             g_last_launches += 2;
         }
+        if (qz && p.qz_late) CK(cudaEventRecord(ws.ev_uv[bsel], stream));
         if (prof) CK(cudaEventRecord(ev[5 * g + 2], stream));
         // ---- Q <- Q U_k, Z <- Z V_k (row chains on the side stream; never read by the chase) ----
         if (qz) {
@@ -620,6 +624,7 @@ int run(int64_t n64, int64_t r64, S* H, int64_t ldh, S* T, int64_t ldt, S* Q, in
     pl.helpers = helpers;
     pl.P = PM;
     pl.nsm = nsm;
+    pl.qz_late = getenv("HT_QZ_LATE") && atoi(getenv("HT_QZ_LATE")) != 0;
     pl.mrg_bytes = mrg_bytes;
     if (comm) {
         pl.comm = comm;
