@@ -42,10 +42,8 @@ __global__ void __launch_bounds__(NT) accum_kernel(AccumArgs<S> a) {
     const int LX = wk | 1;  // odd row stride: thread-per-row access is conflict-free
     S* recs = X + (size_t)wk * LX;  // all qp records of the window, loaded at once
     const int tid = threadIdx.x;
-    for (int e = tid; e < wk * LX; e += NT) {
-        const int l = e / LX, c = e % LX;
-        X[e] = S(l == c ? 1.0 : 0.0);
-    }
+    for (int l = tid / 32; l < wk; l += NT / 32)  // (warp per row, lanes along it: no division)
+        for (int c = tid % 32; c < LX; c += 32) X[(size_t)l * LX + c] = S(l == c ? 1.0 : 0.0);
     if (a.pre)
         for (int t = tid / 32; t < qp; t += NT / 32)  // warp per record (one latency for all of them)
             for (int c = tid % 32; c <= r; c += 32) recs[(size_t)t * (r + 1) + c] = R[((size_t)t * K + k) * (r + 1) + c];
@@ -75,10 +73,9 @@ __global__ void __launch_bounds__(NT) accum_kernel(AccumArgs<S> a) {
         }
         __syncthreads();
     }
-    for (int e = tid; e < a.WP * a.LDB; e += NT) {
-        const int l = e / a.LDB, c = e % a.LDB;
-        Out[e] = (l < wk && c < wk) ? X[(size_t)l * LX + c] : S(0.0);
-    }
+    for (int l = tid / 32; l < a.WP; l += NT / 32)
+        for (int c = tid % 32; c < a.LDB; c += 32)
+            Out[(size_t)l * a.LDB + c] = (l < wk && c < wk) ? X[(size_t)l * LX + c] : S(0.0);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -127,24 +124,22 @@ __global__ void __launch_bounds__(NT) merge_kernel(MergeArgs<S> a) {
         const int o = (khi - klo) * r;
         const int wk = min(w, n - (j1 + khi * r + 1) + 1);
         const S* B = Blk + (size_t)khi * a.WP * a.LDB;
-        for (int e = tid; e < W * LM; e += NT) {
-            const int l = e / LM, c = e % LM;
-            S v = S(0.0);
-            if (c < W) {
-                if (l >= o && l < o + wk && c >= o && c < o + wk) v = B[(size_t)(l - o) * a.LDB + (c - o)];
-                else if (l == c) v = S(1.0);
+        for (int l = tid / 32; l < W; l += NT / 32)
+            for (int c = tid % 32; c < LM; c += 32) {
+                S v = S(0.0);
+                if (c < W) {
+                    if (l >= o && l < o + wk && c >= o && c < o + wk) v = B[(size_t)(l - o) * a.LDB + (c - o)];
+                    else if (l == c) v = S(1.0);
+                }
+                M[(size_t)l * LM + c] = v;
             }
-            M[e] = v;
-        }
     }
     for (int k = khi - 1; k >= klo; --k) {  // M <- M V'_k (columns o .. o+wk)
         const int o = (k - klo) * r;
         const int wk = min(w, n - (j1 + k * r + 1) + 1);
         const S* B = Blk + (size_t)k * a.WP * a.LDB;
-        for (int e = tid; e < wk * wk; e += NT) {
-            const int l = e / wk, c = e % wk;
-            Vs[(size_t)l * LT + c] = B[(size_t)l * a.LDB + c];
-        }
+        for (int l = tid / 32; l < wk; l += NT / 32)
+            for (int c = tid % 32; c < wk; c += 32) Vs[(size_t)l * LT + c] = B[(size_t)l * a.LDB + c];
         __syncthreads();
         // register tiles of 4 rows x 4 columns: 8 shared loads per 16 FMAs (lanes of a warp share
         // the row tile: the M loads broadcast, the Vs loads are consecutive)
@@ -175,14 +170,11 @@ __global__ void __launch_bounds__(NT) merge_kernel(MergeArgs<S> a) {
                     if (l0 + i < W && cb + jj < wk) Tm[(size_t)(l0 + i) * LT + cb + jj] = acc[i][jj];
         }
         __syncthreads();
-        for (int e = tid; e < W * wk; e += NT) {
-            const int l = e / wk, c = e % wk;
-            M[(size_t)l * LM + o + c] = Tm[(size_t)l * LT + c];
-        }
+        for (int l = tid / 32; l < W; l += NT / 32)
+            for (int c = tid % 32; c < wk; c += 32) M[(size_t)l * LM + o + c] = Tm[(size_t)l * LT + c];
         __syncthreads();
     }
-    for (int e = tid; e < a.WP * a.LDB; e += NT) {
-        const int l = e / a.LDB, c = e % a.LDB;
-        Out[e] = (l < W && c < W) ? M[(size_t)l * LM + c] : S(0.0);
-    }
+    for (int l = tid / 32; l < a.WP; l += NT / 32)
+        for (int c = tid % 32; c < a.LDB; c += 32)
+            Out[(size_t)l * a.LDB + c] = (l < W && c < W) ? M[(size_t)l * LM + c] : S(0.0);
 }

@@ -1,9 +1,5 @@
 #!/bin/bash
 cd "$GRAFT_REPO_ROOT" || exit 1
-rm -f gpurun_out/rep.log
-for c in 2 3 4; do
-  for late in 0 1; do
-    HT_QZ_LATE=$late timeout 900 python bench.py --config $c --steps 2 --warmup 3 --no-cpu --no-e2e > gpurun_out/rep_c${c}_$late.json 2>/dev/null
-    python -c "import json; d=json.load(open('gpurun_out/rep_c${c}_$late.json')); print('config $c late $late', round(d['ms_per_step'],2), 'ms/step', d['breakdown_ms'])" >> gpurun_out/rep.log
-  done
-done
+timeout 900 python -m pytest tests/test_gpu_parity.py -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_gpu.log
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"accum|merge" -c 8 --csv --log-file gpurun_out/km.csv python tools/k1prof.py 4096 16 32 > /dev/null 2>&1
+HTARGS="4096,16,32" bash tools/gpu_ht.sh
