@@ -755,22 +755,19 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
         pf_next = false;
         if (t > 0) {
             if (tid == 0) {
-                const int need = min(k + 3, kprev);
-                if (ld_acquire(&a.prog[t - 1]) < need) {
-                    while (ld_relaxed(&a.prog[t - 1]) < need) {
-                    }
-                    (void)ld_acquire(&a.prog[t - 1]);
-                }
+                // sweep t-1 through step k+2 and its helpers through item k+1 (their far strips of
+                // (t-1, k+1) overlap rows >= b0(k-1)): the counters are read with relaxed loads
+                // issued together (one L2 round trip, not one per counter), then one acquire fence
+                const int need = min(k + 3, kprev), hneed = min(k + 2, kprev);
+                const int* hp = hprog + (t - 1) * a.helpers;
+                int v = ld_relaxed(&a.prog[t - 1]);
+                int hv[3] = {hneed, hneed, hneed};
+                for (int h = 0; h < a.helpers && h < 3; ++h) hv[h] = ld_relaxed(hp + h);
+                while (v < need) v = ld_relaxed(&a.prog[t - 1]);
                 K1_TICK(0);
-                for (int h = 0; h < a.helpers; ++h) {  // far strip of (t-1, k+1) overlaps rows >= b0(k-1)
-                    const int hneed = min(k + 2, kprev);
-                    int* hp = &hprog[(t - 1) * a.helpers + h];
-                    if (ld_acquire(hp) < hneed) {
-                        while (ld_relaxed(hp) < hneed) {
-                        }
-                        (void)ld_acquire(hp);
-                    }
-                }
+                for (int h = 0; h < a.helpers && h < 3; ++h)
+                    while (hv[h] < hneed) hv[h] = ld_relaxed(hp + h);
+                asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
                 K1_TICK(9);
             }
             __syncthreads();
