@@ -1,0 +1,41 @@
+"""GPU parity of the alternative schedules the library can be switched to (DESIGN.md §9,
+environment knobs): no far-strip helper CTAs (the chase then owns its whole band), 1 and 3
+helpers, no window merging (K2m off), direct launches instead of the cached graph, and Q/Z
+chains started right after K2.  Each must give the oracle's result like the default path."""
+import os
+
+import pytest
+
+from synth.pencil import make_pencil
+from test_gpu_parity import check_parity
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+VARIANTS = [
+    {"HT_NO_HELPERS": "1"},
+    {"HT_HELPERS": "1"},
+    {"HT_HELPERS": "3"},
+    {"HT_MERGE": "0"},
+    {"HT_NO_GRAPH": "1"},
+    {"HT_QZ_LATE": "0"},
+]
+
+
+@pytest.fixture
+def env(request):
+    saved = {k: os.environ.get(k) for k in request.param}
+    os.environ.update(request.param)
+    yield request.param
+    for k, v in saved.items():
+        if v is None:
+            os.environ.pop(k, None)
+        else:
+            os.environ[k] = v
+
+
+@pytest.mark.parametrize("env", VARIANTS, indirect=True, ids=lambda d: ",".join(f"{k}={v}" for k, v in d.items()))
+@pytest.mark.parametrize("n,r,q,cplx", [(300, 16, 32, False), (257, 64, 9, False), (200, 8, 12, True)])
+def test_variant_parity(env, n, r, q, cplx):
+    H, T = make_pencil(n, r, cplx, seed=97)
+    check_parity(H, T, r, q=q)
