@@ -1,5 +1,7 @@
 #!/bin/bash
 cd "$GRAFT_REPO_ROOT" || exit 1
-timeout 900 python -m pytest tests/test_gpu_parity.py -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_gpu.log
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"accum|merge" -c 8 --csv --log-file gpurun_out/km.csv python tools/k1prof.py 4096 16 32 > /dev/null 2>&1
-HTARGS="4096,16,32" bash tools/gpu_ht.sh
+rm -f gpurun_out/rep.log
+for i in 1 2 3; do
+  timeout 600 python bench.py --steps 3 --warmup 3 --no-cpu > gpurun_out/rep_$i.json 2>/dev/null
+  python -c "import json; d=json.load(open('gpurun_out/rep_$i.json')); print('run $i', round(d['ms_per_step'],2), 'ms/step', round(d['value'],1), 'e2e', round(d['e2e']['value'],1))" >> gpurun_out/rep.log
+done
