@@ -1184,7 +1184,10 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
                 const int nBb = max(0, i2 - i4 + 1);  // B rows i4..i2 (block rows i1..i2 from Cb)
                 const int bn = b0 + r;                 // first row of the next step's column
                 // SPR threads per row (adjacent lanes), CPR columns each, dot by shuffle-xor
-                constexpr int SPR = (MAXM * (int)sizeof(S) > 256) ? MAXM * (int)sizeof(S) / 256 : 1;
+#ifndef HT_STRIP_SPR_BYTES
+#define HT_STRIP_SPR_BYTES 256
+#endif
+                constexpr int SPR = (MAXM * (int)sizeof(S) > HT_STRIP_SPR_BYTES) ? MAXM * (int)sizeof(S) / HT_STRIP_SPR_BYTES : 1;
                 constexpr int CPR = MAXM / SPR;
                 const int part = tid % SPR, c0 = part * CPR;
                 const int nrows = nA + nBb;
