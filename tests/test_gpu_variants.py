@@ -1,7 +1,8 @@
 """GPU parity of the alternative schedules the library can be switched to (DESIGN.md §9,
 environment knobs): no far-strip helper CTAs (the chase then owns its whole band), 1 and 3
 helpers, no window merging (K2m off), direct launches instead of the cached graph, and Q/Z
-chains started right after K2.  Each must give the oracle's result like the default path."""
+chains started right after K2, and the K1 profiler's instrumented path.  Each must give the
+oracle's result like the default path."""
 import os
 
 import pytest
@@ -19,6 +20,7 @@ VARIANTS = [
     {"HT_MERGE": "0"},
     {"HT_NO_GRAPH": "1"},
     {"HT_QZ_LATE": "0"},
+    {"HT_K1PROF": "1", "HT_K1PROF_T": "1"},  # the instrumented path (profile counters, direct launches)
 ]
 
 
