@@ -50,6 +50,7 @@ struct ChainParams {
     int spread;   // > 0 (H/T, two jobs of equal tile count): block order longest chain first (see below)
     long long* prof;  // optional (HT_K1PROF): cycles by phase of one tile's steps (8 slots)
     int prof_tile;    // the profiled tile of job 0 (HT_CHAIN_PROF_TILE)
+    int stair_first;  // right chains: staircase-band tiles dispatched first (HT_STAIR_FIRST=0: off)
 };
 
 // H/T chains are latency-bound by their longest tiles (right updates: the top row tiles walk
@@ -58,11 +59,16 @@ struct ChainParams {
 // interleaved) and block G + x takes the x-th SHORTEST, so an SM's second tile finishes early and
 // leaves the long chain alone on the SM.  Returns (job, tile) of block b.
 inline __host__ __device__ int chain_spread(int nsm) { return nsm > 0 ? nsm : 148; }
+// Right chains: the row tiles of the staircase band [sb0, sb1) (single-window steps with the
+// staircase, measured the slowest) come first, then the others top-down (band0 = band1: plain
+// top-down order).
 __device__ __forceinline__ void chain_order(int b, int total, int spread, bool longest_low, int nt, int& job,
-                                            int& tile) {
+                                            int& tile, int band0 = 0, int band1 = 0) {
     const int rank = (spread > 0 && b >= spread) ? total - 1 - (b - spread) : b;
     job = rank & 1;
-    const int tr = rank >> 1;
+    int tr = rank >> 1;
+    const int nb = band1 - band0;
+    if (longest_low && nb > 0) tr = (tr < nb) ? band0 + tr : ((tr - nb < band0) ? tr - nb : tr);
     tile = longest_low ? tr : nt - 1 - tr;
 }
 
@@ -196,7 +202,12 @@ __device__ __forceinline__ bool chain_tile(const ChainParams<S>& P, int bid, uns
     int jb_ = 0;
     if (P.spread > 0 && P.njobs == 2 && P.job[0].ntiles == P.job[1].ntiles) {
         const int m0 = P.job[0].mode;
-        chain_order(bid, 2 * P.job[0].ntiles, P.spread, m0 == CM_AB_RIGHT, P.job[0].ntiles, jb_, bid);
+        int band0 = 0, band1 = 0;
+        if (m0 == CM_AB_RIGHT && P.stair_first) {  // tiles holding rows j1+1 .. j1+(qp-1) r
+            band0 = min(P.job[0].ntiles, P.j1 / CH_BM);
+            band1 = min(P.job[0].ntiles, (P.j1 + (P.qp - 1) * P.r) / CH_BM + 1);
+        }
+        chain_order(bid, 2 * P.job[0].ntiles, P.spread, m0 == CM_AB_RIGHT, P.job[0].ntiles, jb_, bid, band0, band1);
     } else if (P.njobs > 1 && bid >= P.job[0].ntiles) {
         bid -= P.job[0].ntiles;
         jb_ = 1;

@@ -1,13 +1,10 @@
 #!/bin/bash
 cd "$GRAFT_REPO_ROOT" || exit 1
-rm -f gpurun_out/k1abs.log
-for a in "8192 64 32" "8192 32 32 c" "4096 16 32"; do
-  echo "== base $a" >> gpurun_out/k1abs.log
-  HT_K1PROF=1 HT_K1PROF_T=1 timeout 300 python tools/k1prof.py $a 2>&1 | grep -E "K1 cycles per step|wall" >> gpurun_out/k1abs.log
+timeout 900 python -m pytest tests/test_gpu_parity.py -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_gpu.log
+rm -f gpurun_out/ht.log
+for v in 1 0; do
+  for a in "4096 16 32" "8192 64 32" "8192 32 32 c"; do
+    echo "== STAIR_FIRST=$v $a" >> gpurun_out/ht.log
+    HT_STAIR_FIRST=$v timeout 300 python tools/k1prof.py $a 2>&1 | grep wall | tail -1 >> gpurun_out/ht.log
+  done
 done
-cp exp/libht_stage2.so paper_2301_07964_b200/libht_stage2.so
-for a in "8192 64 32" "8192 32 32 c" "4096 16 32"; do
-  echo "== SPR128 $a" >> gpurun_out/k1abs.log
-  HT_K1PROF=1 HT_K1PROF_T=1 timeout 300 python tools/k1prof.py $a 2>&1 | grep -E "K1 cycles per step|wall" >> gpurun_out/k1abs.log
-done
-timeout 600 python -m pytest tests/test_gpu_parity.py -x -q >> gpurun_out/k1abs.log 2>&1
