@@ -542,6 +542,13 @@ __host__ __device__ inline size_t chase_smem_elems(int r, int qp, int strip_cap)
 // (the same per-row reflector order as Alg. 3): item (t,k) after sweep t's step k (its Z record)
 // and after helper t-1's item k+1 (lag as the sweeps).  Sweep t+1 waits for helper t before its
 // step k-1 (see chase_kernel).
+// The helpers take the band rows above b0(k - HT_HELPER_LAG), lag 1.  Lag 0 (rows [b0(k-1),
+// b0(k)) to the helpers too) would shrink the sweep's band by r rows, but sweep j+1 prefetches
+// its step k-1's B block and y column (which hold some of those rows in window k's first column)
+// during its step k-2, before it has waited for helper j's item k: measured wrong (eB ~ 0.1).
+#ifndef HT_HELPER_LAG
+#define HT_HELPER_LAG 1
+#endif
 template <typename S, int NT, int MAXM>
 __device__ __forceinline__ void far_strip_helper(const ChaseArgs<S>& a, int t, int h, S* sm) {
     const int H = a.helpers;
@@ -582,7 +589,7 @@ __device__ __forceinline__ void far_strip_helper(const ChaseArgs<S>& a, int t, i
         const int i3 = min(j + (k + 2) * r, n);
         const int i4 = j1 + 1 + max(0, (k + t - qp + 1) * r);
         const int m = i2 - i1 + 1;
-        const int cF = j1 + (k - 1) * r + 1;
+        const int cF = j1 + (k - HT_HELPER_LAG) * r + 1;  // rows above b0(k - lag) (see the sweep)
         const int nAf = max(0, min(cF, i3 + 1) - i4), nBf = max(0, min(cF, i2 + 1) - i4);
         if (m >= 2 && nAf + nBf > 0) {
             const S* rec = a.Zr + ((int64_t)t * K + k) * (r + 1);
@@ -784,7 +791,7 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
         const int i3 = min(j + (k + 2) * r, n);
         const int i4g = j1 + 1 + max(0, (k + t - qp + 1) * r);
         // this CTA's part of the band: rows >= b0(k-1) when the helpers take the far rows
-        const int i4 = a.helpers ? max(i4g, j1 + (k - 1) * r + 1) : i4g;
+        const int i4 = a.helpers ? max(i4g, j1 + (k - HT_HELPER_LAG) * r + 1) : i4g;
         const int b0 = j1 + k * r + 1;
         const int m = i2 - i1 + 1;
         const int L = (t > 0) ? min(j - 1 + (k + 1) * r, n) - b0 + 1 : 0;
