@@ -44,6 +44,7 @@ struct ChaseArgs {
                     // own interleaved 64-row blocks of the matrix (hprog[t*H + h])
     long long* prof;  // optional: per-CTA cycle counts of the step phases (12 slots)
     int prof_t0;      // >= 0: only sweep prof_t0 of each group records
+    int hlag;         // helpers take the band rows above b0(k - hlag): 1, or 0 (see far_strip_helper)
 };
 
 __device__ __forceinline__ int ld_acquire(const int* p) {
@@ -542,13 +543,12 @@ __host__ __device__ inline size_t chase_smem_elems(int r, int qp, int strip_cap)
 // (the same per-row reflector order as Alg. 3): item (t,k) after sweep t's step k (its Z record)
 // and after helper t-1's item k+1 (lag as the sweeps).  Sweep t+1 waits for helper t before its
 // step k-1 (see chase_kernel).
-// The helpers take the band rows above b0(k - HT_HELPER_LAG), lag 1.  Lag 0 (rows [b0(k-1),
-// b0(k)) to the helpers too) would shrink the sweep's band by r rows, but sweep j+1 prefetches
-// its step k-1's B block and y column (which hold some of those rows in window k's first column)
-// during its step k-2, before it has waited for helper j's item k: measured wrong (eB ~ 0.1).
-#ifndef HT_HELPER_LAG
-#define HT_HELPER_LAG 1
-#endif
+// The helpers take the band rows above b0(k - hlag) (ChaseArgs::hlag).  Lag 0 also gives them
+// the rows [b0(k-1), b0(k)): sweep j+1 first touches those rows of window k's columns at its
+// step k-1 (one shared column: the last of its B block and its y column) after waiting for
+// helper j's items <= k -- so with lag 0 the y column is loaded at the step start instead of
+// being prefetched during step k-2 (the B block's last column is patched from the caught-up y
+// anyway); sweep j itself never reads those rows again.
 template <typename S, int NT, int MAXM>
 __device__ __forceinline__ void far_strip_helper(const ChaseArgs<S>& a, int t, int h, S* sm) {
     const int H = a.helpers;
@@ -589,7 +589,7 @@ __device__ __forceinline__ void far_strip_helper(const ChaseArgs<S>& a, int t, i
         const int i3 = min(j + (k + 2) * r, n);
         const int i4 = j1 + 1 + max(0, (k + t - qp + 1) * r);
         const int m = i2 - i1 + 1;
-        const int cF = j1 + (k - HT_HELPER_LAG) * r + 1;  // rows above b0(k - lag) (see the sweep)
+        const int cF = j1 + (k - a.hlag) * r + 1;  // rows above b0(k - lag) (see above)
         const int nAf = max(0, min(cF, i3 + 1) - i4), nBf = max(0, min(cF, i2 + 1) - i4);
         if (m >= 2 && nAf + nBf > 0) {
             const S* rec = a.Zr + ((int64_t)t * K + k) * (r + 1);
@@ -729,7 +729,7 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
         tc = now_;                            \
     } while (0)
     // cp.async of step kk's y column, catch-up records, T factor and B block into a buffer set
-    auto issue_step_loads = [&](int kk, S* ysb, S* Cbb, S* recb, S* Tsmb, S* Mb, int th0, int nth) {
+    auto issue_step_loads = [&](int kk, S* ysb, S* Cbb, S* recb, S* Tsmb, S* Mb, int th0, int nth, bool with_y) {
         const int me = tid - th0, mw = me >> 5, nw = nth >> 5;
         if (me < 0 || me >= nth) return;
         const int jbk = j + max(0, (kk - 1) * r + 1);
@@ -738,7 +738,7 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
         const int Lk = (t > 0) ? min(j - 1 + (kk + 1) * r, n) - b0k + 1 : 0;
         const int cBk = i1k + r - 1;
         if (!(jbk <= n && nxk > 0)) return;
-        if (cBk <= n)
+        if (cBk <= n && with_y)
             for (int i = me; i < nxk; i += nth) k1_ld(&ysb[i], &IDX(a.B, a.ldb, b0k + i, cBk));
         if (MK && t > 0 && Lk >= 1) {
             const S* src = a.Mg + (int64_t)kk * a.mst;
@@ -791,7 +791,7 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
         const int i3 = min(j + (k + 2) * r, n);
         const int i4g = j1 + 1 + max(0, (k + t - qp + 1) * r);
         // this CTA's part of the band: rows >= b0(k-1) when the helpers take the far rows
-        const int i4 = a.helpers ? max(i4g, j1 + (k - HT_HELPER_LAG) * r + 1) : i4g;
+        const int i4 = a.helpers ? max(i4g, j1 + (k - a.hlag) * r + 1) : i4g;
         const int b0 = j1 + k * r + 1;
         const int m = i2 - i1 + 1;
         const int L = (t > 0) ? min(j - 1 + (k + 1) * r, n) - b0 + 1 : 0;
@@ -810,7 +810,11 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
         if (jb <= n && nx > 0) {
             if (k == 0)
                 for (int i = tid; i < nx; i += NT) k1_ld(&xcol[i], &IDX(a.A, a.lda, b0 + i, jb));
-            if (!have) issue_step_loads(k, ys, Cb, rec, Tsm, Msm, 0, NT);
+            if (!have) {
+                issue_step_loads(k, ys, Cb, rec, Tsm, Msm, 0, NT, true);
+            } else if (a.hlag == 0 && i1 + r - 1 <= n) {  // y was not prefetched (see far_strip_helper)
+                for (int i = tid; i < nx; i += NT) k1_ld(&ys[i], &IDX(a.B, a.ldb, b0 + i, i1 + r - 1));
+            }
         }
         k1_commit();
         K1_TICK(1);
@@ -1110,7 +1114,8 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
                     // the warps the RQ does not use, if any)
                     constexpr int RQT = rq_nthr<S, MAXM>();
                     issue_step_loads(k + 1, (k & 1) ? ys0 : ys1, (k & 1) ? Cb0 : Cb1, (k & 1) ? rec0 : rec1,
-                                     (k & 1) ? Tsm0 : Tsm1, (k & 1) ? Msm0 : Msm1, RQT < NT ? RQT : 0, RQT < NT ? NT - RQT : NT);
+                                     (k & 1) ? Tsm0 : Tsm1, (k & 1) ? Msm0 : Msm1, RQT < NT ? RQT : 0, RQT < NT ? NT - RQT : NT,
+                                     a.hlag != 0);
                     asm volatile("cp.async.commit_group;\n" ::: "memory");
                     pf_next = true;
                 }

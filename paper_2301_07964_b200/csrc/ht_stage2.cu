@@ -169,11 +169,12 @@ struct Plan {
     int P = 1;        // window merge factor of the apply chains (K2m)
     int nsm = 148;    // SMs (longest-chain-first tile order of the H/T chains)
     bool qz_late = true;   // Q/Z chains of a group start after its H/T chains (HT_QZ_LATE=0: after K2)
+    int hlag = 1;          // helper row split (ChaseArgs::hlag): 0 for r >= 64 (HT_HELPER_LAG overrides)
     size_t mrg_bytes = 0;
     bool is_root() const { return comm == nullptr || rank == root; }
     bool qz() const { return Q || Z; }
     bool same(const Plan& o) const {
-        return n == o.n && r == o.r && q == o.q && strip_cap == o.strip_cap && helpers == o.helpers && P == o.P && qz_late == o.qz_late && H == o.H && ldh == o.ldh &&
+        return n == o.n && r == o.r && q == o.q && strip_cap == o.strip_cap && helpers == o.helpers && P == o.P && qz_late == o.qz_late && hlag == o.hlag && H == o.H && ldh == o.ldh &&
                T == o.T && ldt == o.ldt && Q == o.Q && ldq == o.ldq && Z == o.Z && ldz == o.ldz;
     }
 };
@@ -368,7 +369,8 @@ int enqueue_groups(const Plan<S>& p, Workspace<S>& ws, cudaStream_t stream, bool
             CK(cudaMemsetAsync(ws.Zr, 0, (size_t)qp * K * (r + 1) * sizeof(S), stream));
             ChaseArgs<S> ca{n, r, qp, j1, K, p.H, p.ldh, p.T, p.ldt, ws.Qr, ws.Zr, ws.Tr, TLD, ws.Mg,
                             mcatch_ld(q, r), mcatch_st(q, r), ws.prog, p.strip_cap,
-                            p.helpers, ws.k1prof, getenv("HT_K1PROF_T") ? atoi(getenv("HT_K1PROF_T")) : -1};
+                            p.helpers, ws.k1prof, getenv("HT_K1PROF_T") ? atoi(getenv("HT_K1PROF_T")) : -1,
+                            p.hlag};
             void* kargs[] = {&ca};
             CK(cudaLaunchKernel(p.chase_fn, dim3(qp * (1 + p.helpers)), dim3(CHASE_NT), kargs, p.chase_bytes, stream));
         }
@@ -625,6 +627,7 @@ int run(int64_t n64, int64_t r64, S* H, int64_t ldh, S* T, int64_t ldt, S* Q, in
     pl.helpers = helpers;
     pl.P = PM;
     pl.nsm = nsm;
+    pl.hlag = getenv("HT_HELPER_LAG") ? (atoi(getenv("HT_HELPER_LAG")) == 0 ? 0 : 1) : (r >= 64 ? 0 : 1);
     // (measured: configs 2 / 3 / 4 -0.8 / -0.3 / -1.1 % per step; HT_QZ_LATE=0 restores the early start)
     pl.qz_late = !(getenv("HT_QZ_LATE") && atoi(getenv("HT_QZ_LATE")) == 0);
     pl.mrg_bytes = mrg_bytes;
