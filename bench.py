@@ -90,13 +90,14 @@ def _ncu_traffic(kernel, n, r, q):
 
 
 class ClockSampler:
-    """SM clocks and throttling DURING the timed region (B200_PROFILING.md), through NVML
-    in-process with as few driver queries as possible (frequent NVML / nvidia-smi polling was
-    measured to stall the host side of the timed loop now and then, +10-20 % on a step):
-    - the power and thermal violation-time counters (cumulative, ns) before and after the region:
-      any increase means the region was throttled (reported as sw_power_cap / *_thermal_slowdown);
-    - the SM clock and the current event-reason bits sampled once 100 ms into the region and once
-      at its end.
+    """SM clocks and throttling over the timed region (B200_PROFILING.md), through NVML
+    in-process and WITHOUT queries inside the region (NVML / nvidia-smi queries during it were
+    measured to stall the host side of the timed loop now and then, up to +0.9 s):
+    - the power and thermal violation-time counters (cumulative, ns) just before and just after
+      the region: any increase means the region was throttled (reported as sw_power_cap /
+      sw_thermal_slowdown);
+    - the SM clock and the current event-reason bits sampled just before and at the end of the
+      region (the GPU is still at its load clock then).
     nvidia-smi is the fallback when NVML is unavailable."""
 
     Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
@@ -143,8 +144,7 @@ class ClockSampler:
             except Exception:
                 self.mx = 0.0
             self.v0 = self._violations()
-            self.th = threading.Thread(target=self._poll, daemon=True)
-            self.th.start()
+            self._sample()
             return
         except Exception:
             self.nvml = None
@@ -157,18 +157,12 @@ class ClockSampler:
         except Exception:
             self.proc = None
 
-    def _poll(self):
-        if not self.stop_ev.wait(0.1):
-            self._sample()
-
     def _read(self):
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
     def stop(self):
         if self.nvml is not None:
-            self.stop_ev.set()
-            self.th.join(timeout=5)
             nv = self.nvml
             self._sample()
             v1 = self._violations()
@@ -320,9 +314,13 @@ def main():
         Zd.copy_(I0)
         ht.ht_stage2(H, T, r, Qd, Zd, stream=stream, q=q, profile=profile, comm=comm)
 
-    for _ in range(max(3, args.warmup)):
+    # warm-up: at least W steps and at least 3 s of work -- the first seconds of a fresh process
+    # on a fresh box were measured up to 25 % slower (clock / power ramp)
+    n_warm, t_warm = 0, time.time()
+    while n_warm < max(3, args.warmup) or time.time() - t_warm < 3.0:
         step()
-    torch.cuda.synchronize()
+        torch.cuda.synchronize()
+        n_warm += 1
     # one profiled call (per-kernel-class device times via events) outside the timed region
     step(profile=True)
     torch.cuda.synchronize()
@@ -390,7 +388,7 @@ def main():
 
     out = {
         "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
-        "warmup": max(3, args.warmup), "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+        "warmup": n_warm, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64" if not cplx else "c128", "data": "synthetic",
         "config": _config_dict(args, c, q),
         "roofline": roof,
@@ -417,7 +415,8 @@ def main():
             for o, X in zip(outs, (H, T, Qd, Zd)):
                 o.copy_(X.t(), non_blocking=True)
 
-        e2e_step()  # untimed: first transfers from / to the freshly pinned buffers
+        for _ in range(2):  # untimed: first transfers from / to the freshly pinned buffers
+            e2e_step()
         barrier()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
