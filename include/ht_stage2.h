@@ -26,8 +26,12 @@
  * pointer is dereferenced after the work enqueued by the call completes.
  *
  * Streams: stream-ordered on `stream` (like cuSOLVER).  Internal streams are
- * joined back to `stream` with events.  The host blocks once at entry (input
- * validation) and may block at exit.
+ * joined back to `stream` with events.  The input check (a kernel) and the
+ * reduction are both enqueued before the host waits, and it waits only for the
+ * check (so for the work already on `stream` ahead of it): on return the
+ * reduction may still be running.  On an input error the reduction has run on
+ * the rejected buffers too and their contents are undefined.  Profiling and
+ * multi-GPU calls may also block at exit.
  *
  * Q == NULL or Z == NULL skips that accumulation; H and T are then bitwise
  * identical to an accumulating run.

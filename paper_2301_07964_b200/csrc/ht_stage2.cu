@@ -552,27 +552,54 @@ int run(int64_t n64, int64_t r64, S* H, int64_t ldh, S* T, int64_t ldt, S* Q, in
     const int n = (int)n64;
     const int r = (int)std::min<int64_t>(r64, std::max<int64_t>(1, n64));
     const bool prof = getenv("HT_PROFILE") != nullptr || (opts && (opts->flags & HT_FLAG_PROFILE));
-    cudaEvent_t e_start, e_end;
-    CK(cudaEventCreate(&e_start));
-    CK(cudaEventCreate(&e_end));
-    CK(cudaEventRecord(e_start, stream));
+    cudaEvent_t e_start = nullptr, e_end = nullptr;
+    if (prof) {
+        CK(cudaEventCreate(&e_start));
+        CK(cudaEventCreate(&e_end));
+        CK(cudaEventRecord(e_start, stream));
+    }
 
-    // ---- K5: input validation (exact structure + finiteness), host blocks once ----
-    if (!(opts && (opts->flags & HT_FLAG_NO_VALIDATE))) {
-        unsigned long long* flags = nullptr;
-        CK(cudaMallocAsync(&flags, 2 * sizeof(unsigned long long), stream));
-        CK(cudaMemsetAsync(flags, 0, 2 * sizeof(unsigned long long), stream));
-        validate_kernel<S><<<4 * 148, 256, 0, stream>>>(n, r, H, ldh, T, ldt, Q, ldq, Z, ldz, flags);
+    // ---- K5: input validation (exact structure + finiteness) ----
+    // The reduction is enqueued right behind the check and the host then waits for the check
+    // only: the call returns its verdict while the reduction runs, so back-to-back calls keep
+    // the GPU busy (on invalid input the reduction's outputs are undefined, as the header says).
+    struct ValState {
+        unsigned long long* dflags = nullptr;  // device
+        unsigned long long* hflags = nullptr;  // pinned host
+        cudaEvent_t done = nullptr;
+        int dev = -1;
+    };
+    static thread_local ValState vs;
+    const bool validate = !(opts && (opts->flags & HT_FLAG_NO_VALIDATE));
+    if (validate) {
+        int dev = 0;
+        CK(cudaGetDevice(&dev));
+        if (vs.dev != dev) {  // (per host thread and device; the old device's state is dropped)
+            CK(cudaMalloc(&vs.dflags, 2 * sizeof(unsigned long long)));
+            CK(cudaMallocHost(&vs.hflags, 2 * sizeof(unsigned long long)));
+            CK(cudaEventCreateWithFlags(&vs.done, cudaEventDisableTiming));
+            vs.dev = dev;
+        }
+        CK(cudaMemsetAsync(vs.dflags, 0, 2 * sizeof(unsigned long long), stream));
+        validate_kernel<S><<<4 * 148, 256, 0, stream>>>(n, r, H, ldh, T, ldt, Q, ldq, Z, ldz, vs.dflags);
         ++g_last_launches;
         CK(cudaGetLastError());
-        unsigned long long hf[2] = {0, 0};
-        CK(cudaMemcpyAsync(hf, flags, sizeof(hf), cudaMemcpyDeviceToHost, stream));
-        CK(cudaFreeAsync(flags, stream));
-        CK(cudaStreamSynchronize(stream));
-        if (hf[0]) return HT_ESTRUCT;
-        if (hf[1]) return HT_ENONFINITE;
+        CK(cudaMemcpyAsync(vs.hflags, vs.dflags, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, stream));
+        CK(cudaEventRecord(vs.done, stream));
     }
-    if (n <= 2 || r <= 1) return HT_OK;  // exact no-op
+    auto verdict = [&]() -> int {
+        if (!validate) return HT_OK;
+        CK(cudaEventSynchronize(vs.done));
+        if (vs.hflags[0]) return HT_ESTRUCT;
+        if (vs.hflags[1]) return HT_ENONFINITE;
+        return HT_OK;
+    };
+    if (n <= 2 || r <= 1) return verdict();  // exact no-op
+    // a call refused before any launch still reports an input error first
+    auto refuse = [&](int code) -> int {
+        const int v = verdict();
+        return v ? v : code;
+    };
 
     int64_t q64 = (opts && opts->q > 0) ? opts->q : default_q(n, r, is_complex);
     const int q = (int)std::max<int64_t>(1, std::min<int64_t>(q64, n - 2));
@@ -603,7 +630,7 @@ int run(int64_t n64, int64_t r64, S* H, int64_t ldh, S* T, int64_t ldt, S* Q, in
     const bool acc_pre = accum_smem_bytes<S>(r, q, true) <= 200 * 1024;
     const size_t acc_bytes = accum_smem_bytes<S>(r, q, acc_pre);
     const void* chase_fn = chase_kernel_for<S>(r);
-    if (!chase_fn || q > 148) return HT_EUNSUPPORTED;  // one co-resident CTA per sweep
+    if (!chase_fn || q > 148) return refuse(HT_EUNSUPPORTED);  // one co-resident CTA per sweep
     const size_t ch_bytes = chain_bytes_rt<S>(WP, r, q, PM);
     const size_t mrg_bytes = PM > 1 ? merge_smem_bytes<S>(Wm, w) : 0;
     int dev = 0, smem_optin = 0, nsm = 0;
@@ -612,12 +639,12 @@ int run(int64_t n64, int64_t r64, S* H, int64_t ldh, S* T, int64_t ldt, S* Q, in
     CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
     if (chase_bytes > (size_t)smem_optin || ch_bytes > (size_t)smem_optin || acc_bytes > (size_t)smem_optin ||
         mrg_bytes > (size_t)smem_optin)
-        return HT_EUNSUPPORTED;
+        return refuse(HT_EUNSUPPORTED);
     if (PM > 1) CK(cudaFuncSetAttribute(merge_kernel<S, ACC_NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mrg_bytes));
     CK(cudaFuncSetAttribute(chase_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)chase_bytes));
     CK(cudaFuncSetAttribute(accum_kernel<S, ACC_NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)acc_bytes));
 
-    if (int rcp = chain_prepare<S>(WP)) return rcp;
+    if (int rcp = chain_prepare<S>(WP)) return refuse(rcp);
     // far-strip helpers per sweep: as many as fit next to the q sweeps, at most 3 (HT_HELPERS)
     int helpers = std::max(0, std::min(3, nsm / q - 2));  // q=32: 2, q<=21: 3
     if (getenv("HT_HELPERS")) helpers = std::max(0, std::min(3, atoi(getenv("HT_HELPERS"))));
@@ -636,7 +663,7 @@ int run(int64_t n64, int64_t r64, S* H, int64_t ldh, S* T, int64_t ldt, S* Q, in
         NK(ncclCommCount(comm, &pl.nranks));
         NK(ncclCommUserRank(comm, &pl.rank));
         pl.root = opts ? opts->root : 0;
-        if (pl.root < 0 || pl.root >= pl.nranks) return -13;
+        if (pl.root < 0 || pl.root >= pl.nranks) return refuse(-13);
     } else if (opts && (opts->flags & HT_FLAG_EMULATE_SLABS)) {
         pl.emul = std::max(1, opts->reserved[0]);
     }
@@ -649,6 +676,7 @@ int run(int64_t n64, int64_t r64, S* H, int64_t ldh, S* T, int64_t ldt, S* Q, in
         rc = enqueue_groups<S>(pl, ws, stream, prof);
         if (int rf = ws.release(stream, /*async=*/true)) rc = rc ? rc : rf;
         if (rc) return rc;
+        if (int rv = verdict()) return rv;
         if (k1p) print_k1prof(ws.k1prof_host);
     } else {
         // the whole group loop as one cached CUDA graph (one launch per call; no host stalls)
@@ -656,16 +684,17 @@ int run(int64_t n64, int64_t r64, S* H, int64_t ldh, S* T, int64_t ldt, S* Q, in
         if ((rc = graph_for<S>(pl, stream, &ge))) return rc;
         CK(cudaGraphLaunch(ge->exec, stream));
         g_last_launches += ge->launches;
+        if (int rv = verdict()) return rv;
     }
-    CK(cudaEventRecord(e_end, stream));
     if (prof) {
+        CK(cudaEventRecord(e_end, stream));
         CK(cudaEventSynchronize(e_end));
         float tot = 0;
         CK(cudaEventElapsedTime(&tot, e_start, e_end));
         g_last_ms[3] = tot;
+        cudaEventDestroy(e_start);
+        cudaEventDestroy(e_end);
     }
-    cudaEventDestroy(e_start);
-    cudaEventDestroy(e_end);
     CK(cudaGetLastError());
     return HT_OK;
 }

@@ -188,6 +188,9 @@ def test_error_codes():
     with pytest.raises(ht.HTError) as e:
         ht.ht_stage2(Hd, _dev(T), -1)
     assert e.value.code == -2
+    # the rejected calls' reductions were enqueued behind the check (header: outputs undefined);
+    # they must leave the library in a state where the next valid call is exact
+    check_parity(H, T, 4)
 
 
 # ---------------------------------------------------------------------------- multi-GPU decomposition
