@@ -169,7 +169,7 @@ struct Plan {
     int P = 1;        // window merge factor of the apply chains (K2m)
     int nsm = 148;    // SMs (longest-chain-first tile order of the H/T chains)
     bool qz_late = true;   // Q/Z chains of a group start after its H/T chains (HT_QZ_LATE=0: after K2)
-    int hlag = 1;          // helper row split (ChaseArgs::hlag): 0 for r >= 64 (HT_HELPER_LAG overrides)
+    int hlag = 1;          // helper row split (ChaseArgs::hlag): 0 for r >= 32 (HT_HELPER_LAG overrides)
     size_t mrg_bytes = 0;
     bool is_root() const { return comm == nullptr || rank == root; }
     bool qz() const { return Q || Z; }
@@ -654,7 +654,7 @@ int run(int64_t n64, int64_t r64, S* H, int64_t ldh, S* T, int64_t ldt, S* Q, in
     pl.helpers = helpers;
     pl.P = PM;
     pl.nsm = nsm;
-    pl.hlag = getenv("HT_HELPER_LAG") ? (atoi(getenv("HT_HELPER_LAG")) == 0 ? 0 : 1) : (r >= 64 ? 0 : 1);
+    pl.hlag = getenv("HT_HELPER_LAG") ? (atoi(getenv("HT_HELPER_LAG")) == 0 ? 0 : 1) : (r >= 32 ? 0 : 1);
     // (measured: configs 2 / 3 / 4 -0.8 / -0.3 / -1.1 % per step; HT_QZ_LATE=0 restores the early start)
     pl.qz_late = !(getenv("HT_QZ_LATE") && atoi(getenv("HT_QZ_LATE")) == 0);
     pl.mrg_bytes = mrg_bytes;

@@ -20,7 +20,7 @@ VARIANTS = [
     {"HT_MERGE": "0"},
     {"HT_NO_GRAPH": "1"},
     {"HT_QZ_LATE": "0"},
-    {"HT_HELPER_LAG": "0"},  # helpers also take the rows just above b0(k) (default only for r >= 64)
+    {"HT_HELPER_LAG": "0"},  # helpers also take the rows just above b0(k) (default only for r >= 32)
     {"HT_HELPER_LAG": "1"},
     {"HT_K1PROF": "1", "HT_K1PROF_T": "1"},  # the instrumented path (profile counters, direct launches)
 ]
