@@ -89,6 +89,27 @@ def _ncu_traffic(kernel, n, r, q):
     return None
 
 
+def _invariants_dev(A, B, H, T, Q, Z):
+    """north_star's bounds on the GPU in fp64 (torch matmuls; a check, not the product path):
+    ||A - QHZ*||_F/||A||_F, same for B, ||Q*Q - I||_F, ||Z*Z - I||_F, each also / (10 n u), and
+    the count of entries that must be exactly zero but are not."""
+    import torch
+    n = A.shape[0]
+    Zh = Z.conj().t()
+    eA = float(torch.linalg.norm(A - Q @ (H @ Zh)) / torch.linalg.norm(A))
+    eB = float(torch.linalg.norm(B - Q @ (T @ Zh)) / torch.linalg.norm(B))
+    I = torch.eye(n, dtype=A.dtype, device=A.device)
+    oQ = float(torch.linalg.norm(Q.conj().t() @ Q - I))
+    oZ = float(torch.linalg.norm(Zh @ Z - I))
+    del I, Zh
+    zeros = int(torch.count_nonzero(torch.tril(H, -2))) + int(torch.count_nonzero(torch.tril(T, -1)))
+    bound = 10.0 * n * 2.0 ** -53
+    torch.cuda.empty_cache()
+    return {"eA": eA, "eB": eB, "oQ": oQ, "oZ": oZ, "bound": bound,
+            "over_bound": {k: v / bound for k, v in (("eA", eA), ("eB", eB), ("oQ", oQ), ("oZ", oZ))},
+            "zeros_bad": zeros, "pass": max(eA, eB, oQ, oZ) <= bound and zeros == 0}
+
+
 class ClockSampler:
     """SM clocks and throttling over the timed region (B200_PROFILING.md), through NVML
     in-process and WITHOUT queries inside the region (NVML / nvidia-smi queries during it were
@@ -105,8 +126,9 @@ class ClockSampler:
          "clocks_event_reasons.sw_power_cap")
     NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
-    def __init__(self, index: int):
+    def __init__(self, index: int, interval: float = 0.0):
         self.index = index
+        self.interval = interval
         self.proc = None
         self.nvml = None
         self.lines = []
@@ -145,6 +167,9 @@ class ClockSampler:
                 self.mx = 0.0
             self.v0 = self._violations()
             self._sample()
+            if self.interval > 0:  # sampled DURING the region too (long steps hide host stalls)
+                self.th = threading.Thread(target=self._loop, daemon=True)
+                self.th.start()
             return
         except Exception:
             self.nvml = None
@@ -157,6 +182,10 @@ class ClockSampler:
         except Exception:
             self.proc = None
 
+    def _loop(self):
+        while not self.stop_ev.wait(self.interval):
+            self._sample()
+
     def _read(self):
         for line in self.proc.stdout:
             self.lines.append(line.strip())
@@ -164,6 +193,9 @@ class ClockSampler:
     def stop(self):
         if self.nvml is not None:
             nv = self.nvml
+            self.stop_ev.set()
+            if getattr(self, "th", None) is not None:
+                self.th.join(timeout=5)
             self._sample()
             v1 = self._violations()
             bits = {"hw_slowdown": nv.nvmlClocksEventReasonHwSlowdown,
@@ -207,33 +239,55 @@ class ClockSampler:
 
 
 def cpu_sample(cfg, n_s):
-    """Oracle (plain C Alg. 2, all host cores) on the leading n_s x n_s sub-pencil of config cfg."""
+    """Oracle (plain C Alg. 2, all host cores) on the leading n_s x n_s sub-pencil of config cfg.
+    Returns (GFLOP/s at 10 n_s^3, threads used, seconds, CPU seconds / wall seconds)."""
     import oracle
     c = CONFIGS[cfg]
     H, T = make_pencil(c["n"] if c["n"] <= 4096 else n_s, c["r"], c["complex"], c["tdiag"], c["seed"])
     H = np.asfortranarray(H[:n_s, :n_s])
     T = np.asfortranarray(T[:n_s, :n_s])
     cores = oracle.set_threads(len(os.sched_getaffinity(0)))
+    c0 = time.process_time()
     t0 = time.perf_counter()
     oracle.stage2(H, T, c["r"])
     dt = time.perf_counter() - t0
+    par = (time.process_time() - c0) / max(dt, 1e-9)  # effective parallelism actually used
     fl = (40.0 if c["complex"] else 10.0) * n_s ** 3
-    return fl / dt / 1e9, cores, dt
+    return fl / dt / 1e9, cores, dt, par
+
+
+def _full_oracle_record(cfg):
+    """The oracle's own full-size run on this config, if tools/oracle_cache.py cached it
+    (builder container; not the GPU box): seconds, threads, invariants, noise floor."""
+    try:
+        d = np.load(os.path.join(ROOT, "oracle_cache", f"cfg{cfg}.npz"))
+        m = json.loads(str(d["meta"]))
+        fl = (40.0 if m["complex"] else 10.0) * m["n"] ** 3
+        return {"seconds": m["oracle_s"], "threads": m["oracle_threads"], "gflops": fl / m["oracle_s"] / 1e9,
+                "host": "builder container (tools/oracle_cache.py), not the GPU box", "noise_floor": m.get("floor")}
+    except Exception:
+        return None
+
+
+def _sample_n(c):
+    """Leading sub-pencil size of the CPU samples (about 10-30 s of oracle work on 8-16 cores)."""
+    return min(c["n"], 1536 if c["complex"] else 2048)
 
 
 def run_reference(args, rank):
     if rank != 0:
         return
     c = CONFIGS[args.config]
-    n_s = args.sample_n or min(c["n"], 1536 if c["complex"] else 2048)
+    n_s = args.sample_n or _sample_n(c)
     for _ in range(args.warmup):
         cpu_sample(args.config, min(n_s, 512))
-    vals, times = [], []
+    vals, times, pars = [], [], []
     cores = 1
     for _ in range(args.steps):
-        v, cores, dt = cpu_sample(args.config, n_s)
+        v, cores, dt, par = cpu_sample(args.config, n_s)
         vals.append(v)
         times.append(dt)
+        pars.append(par)
     v = statistics.mean(vals)
     sample = (f"oracle (Alg. 2, plain C, OpenMP) full reduction of the leading {n_s}x{n_s} sub-pencil "
               f"of config{args.config} (r={c['r']}, same generator/seed); rate = 10n_s^3/t")
@@ -242,7 +296,9 @@ def run_reference(args, rank):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.mean(times),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64" if not c["complex"] else "c128",
         "data": "synthetic", "config": _config_dict(args, c, q=None),
-        "cpu_baseline": {"value": v, "unit": "GFLOP/s", "cores": cores, "kind": "oracle", "sample": sample},
+        "cpu_baseline": {"value": v, "unit": "GFLOP/s", "cores": cores, "kind": "oracle", "sample": sample,
+                         "effective_parallelism": statistics.mean(pars),
+                         "full_config_oracle": _full_oracle_record(args.config)},
         "e2e": {"value": v, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
 
@@ -263,12 +319,13 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--q", type=int, default=0)
     ap.add_argument("--sample-n", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-check", action="store_true")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -330,7 +387,9 @@ def main():
         if world > 1:
             dist.barrier()
 
-    clocks = ClockSampler(local)
+    # steps of a second or more: NVML samples every 0.5 s inside the region (a host stall there
+    # is hidden by the queued work); shorter steps: only at both ends (see ClockSampler)
+    clocks = ClockSampler(local, interval=0.5 if brk_ms["total"] > 1000.0 else 0.0)
     barrier()
     torch.cuda.synchronize()
     clocks.start()
@@ -400,6 +459,10 @@ def main():
         "measured_peaks": {k: peaks.get(k) for k in ("hbm_gbs", "bf16_tflops")},
     }
 
+    # ---- result check of the last timed step (north_star invariants; test-side fp64 torch matmuls) ----
+    if not args.no_check:
+        out["invariants"] = _invariants_dev(H0, T0, H, T, Qd, Zd)
+
     # ---- end to end: host pinned buffers -> device, C-ABI call, results -> host ----
     if not args.no_e2e:
         hp = [torch.from_numpy(A.T.copy()).pin_memory() for A in (H_np, T_np)]  # row-major of A^T
@@ -435,12 +498,13 @@ def main():
                       "h2d_bytes_per_step": 4 * n * n * esz, "d2h_bytes_per_step": 4 * n * n * esz}
 
     if rank == 0 and not args.no_cpu:
-        n_s = args.sample_n or min(n, 1536 if cplx else 2048)
-        v, cores, dt = cpu_sample(args.config, n_s)
+        n_s = args.sample_n or _sample_n(c)
+        v, cores, dt, par = cpu_sample(args.config, n_s)
         out["cpu_baseline"] = {
-            "value": v, "unit": "GFLOP/s", "cores": cores, "kind": "oracle",
+            "value": v, "unit": "GFLOP/s", "cores": cores, "kind": "oracle", "effective_parallelism": par,
             "sample": f"oracle (Alg. 2, plain C, OpenMP) full reduction of the leading {n_s}x{n_s} sub-pencil of "
-                      f"config{args.config} (r={r}); {dt:.1f} s; rate = 10n_s^3/t"}
+                      f"config{args.config} (r={r}); {dt:.1f} s; rate = 10n_s^3/t",
+            "full_config_oracle": _full_oracle_record(args.config)}
     if rank == 0:
         print(json.dumps(out), flush=True)
     if world > 1:

@@ -21,17 +21,24 @@
  * path replays a CUDA graph of the whole reduction that the library caches per
  * host thread, keyed by (device, n, r, q, buffer pointers and leading
  * dimensions); each cached graph owns its workspace (plain cudaMalloc, at most 4
- * entries, the oldest evicted).  Profiling and multi-GPU calls allocate
- * workspace stream-ordered on `stream` and free it before return.  No caller
- * pointer is dereferenced after the work enqueued by the call completes.
+ * entries, the oldest evicted) and holds the caller's pointers only as replay
+ * arguments: it never touches the buffers outside a call.  ht_release_cache()
+ * frees every cached graph, its workspace and the input-check state of the
+ * calling thread (call it before freeing buffers a cached graph was built on if
+ * the same addresses may be reused for other data, or to return the memory).
+ * Profiling and multi-GPU calls allocate workspace stream-ordered on `stream`
+ * and free it before return.  No caller pointer is dereferenced after the work
+ * enqueued by the call completes.
  *
  * Streams: stream-ordered on `stream` (like cuSOLVER).  Internal streams are
- * joined back to `stream` with events.  The input check (a kernel) and the
+ * joined back to `stream` with events.  The input check (a kernel, K5) and the
  * reduction are both enqueued before the host waits, and it waits only for the
  * check (so for the work already on `stream` ahead of it): on return the
- * reduction may still be running.  On an input error the reduction has run on
- * the rejected buffers too and their contents are undefined.  Profiling and
- * multi-GPU calls may also block at exit.
+ * reduction may still be running.  Every kernel of the reduction first reads the
+ * check's verdict on the device and exits at once if the input was rejected, so
+ * on return codes 1 and 2 H, T, Q and Z are unchanged (the caller may clean the
+ * input, e.g. flush roundoff below the band, and retry on the same buffers).
+ * Profiling and multi-GPU calls may also block at exit.
  *
  * Q == NULL or Z == NULL skips that accumulation; H and T are then bitwise
  * identical to an accumulating run.
@@ -49,8 +56,9 @@
  *   -i  argument i invalid (1-based position: n < 0, r < 0, null H/T,
  *       ld < max(1,n)); returned synchronously, nothing launched
  *    1  input violates the r-HT structure (nonzero below H's r-th subdiagonal
- *       or below T's diagonal) -- checked exactly on the device before work
- *    2  input has a non-finite entry (NaN/Inf) in H, T, Q or Z
+ *       or below T's diagonal) -- checked exactly on the device before any
+ *       work; the buffers are left unchanged
+ *    2  input has a non-finite entry (NaN/Inf) in H, T, Q or Z (buffers unchanged)
  *    3  CUDA error   4  NCCL error   5  out of device memory
  *    6  configuration not supported by this build (e.g. shared-memory limits)
  * No partial results are promised on error.
@@ -75,12 +83,13 @@ extern "C" {
 
 /* Tunables (NULL = defaults).  q: sweeps per group ("q");
  * 0 = default (environment HT_Q, else a per-r choice documented in DESIGN.md).
- * chase_ctas: reserved (the chase runs one CTA per sweep plus far-strip helpers).
+ * reserved0: ignored, must be 0 (the chase always runs one CTA per sweep of a
+ * group plus far-strip helper CTAs).
  * root: result rank for comm != NULL.  flags: bit 0 = skip input validation,
  * bit 1 = record per-kernel-class device times (see ht_last_timing). */
 typedef struct ht_opts {
     int64_t q;
-    int32_t chase_ctas;
+    int32_t reserved0;
     int32_t root;
     int32_t flags;
     int32_t reserved[5];
@@ -114,6 +123,10 @@ int ht_stage2_z_ex(int64_t n, int64_t r, cuDoubleComplex *H, int64_t ldh, cuDoub
 int ht_nccl_unique_id(void *id_out);
 int ht_comm_create(const void *id, int rank, int nranks, ncclComm_t *out);
 int ht_comm_destroy(ncclComm_t comm);
+
+/* Frees the calling host thread's cached CUDA graphs with their workspace and its input-check
+ * state on every device (synchronises those devices first).  Returns 0 or 3 (CUDA error). */
+int ht_release_cache(void);
 
 /* Multi-GPU row slab: rows [*row0, *row0 + *nrows) (0-based) of Q and Z are updated
  * by `rank` of `nranks` (whole 32-row tiles, balanced).  Host-only; returns 0 or -i. */

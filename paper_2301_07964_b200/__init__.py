@@ -16,7 +16,8 @@ import ctypes
 import os
 
 __all__ = ["ht_stage2", "ht_stage2_host", "HTError", "flops_std", "default_q", "strerror",
-           "last_timing", "probe_dmma_tflops", "probe_dfma_tflops", "library_path", "Opts"]
+           "last_timing", "probe_dmma_tflops", "probe_dfma_tflops", "library_path", "Opts",
+           "release_cache"]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SO = os.path.join(_HERE, "libht_stage2.so")
@@ -30,7 +31,7 @@ class HTError(RuntimeError):
 
 
 class Opts(ctypes.Structure):
-    _fields_ = [("q", ctypes.c_int64), ("chase_ctas", ctypes.c_int32), ("root", ctypes.c_int32),
+    _fields_ = [("q", ctypes.c_int64), ("reserved0", ctypes.c_int32), ("root", ctypes.c_int32),
                 ("flags", ctypes.c_int32), ("reserved", ctypes.c_int32 * 5)]
 
 
@@ -73,6 +74,8 @@ def _load():
     lib.ht_comm_destroy.restype = ctypes.c_int
     lib.ht_slab_range.argtypes = [i64, ctypes.c_int, ctypes.c_int, ctypes.POINTER(i64), ctypes.POINTER(i64)]
     lib.ht_slab_range.restype = ctypes.c_int
+    lib.ht_release_cache.argtypes = []
+    lib.ht_release_cache.restype = ctypes.c_int
     _lib = lib
     return lib
 
@@ -80,7 +83,7 @@ def _load():
 EXPORTED_SYMBOLS = ("ht_stage2_d", "ht_stage2_z", "ht_stage2_d_ex", "ht_stage2_z_ex",
                     "ht_nccl_unique_id", "ht_comm_create", "ht_comm_destroy", "ht_slab_range", "ht_strerror",
                     "ht_flops_std", "ht_default_q", "ht_last_timing", "ht_probe_dmma_tflops",
-                    "ht_probe_dfma_tflops")
+                    "ht_probe_dfma_tflops", "ht_release_cache")
 
 
 def slab_range(n: int, nranks: int, rank: int):
@@ -118,6 +121,14 @@ def comm_from_torch(group=None):
     obj = [nccl_unique_id() if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0, group=group)
     return nccl_comm(rank, world, obj[0])
+
+
+def release_cache() -> None:
+    """Free this thread's cached CUDA graphs, their workspace and the input-check state (C ABI
+    ``ht_release_cache``)."""
+    rc = _load().ht_release_cache()
+    if rc != 0:
+        raise HTError(rc)
 
 
 def comm_destroy(comm) -> None:
@@ -167,7 +178,7 @@ def _check_mat(X, n, name, dtype):
     return ctypes.c_void_p(X.data_ptr()), max(1, X.stride(1) if n > 1 else n)
 
 
-def ht_stage2(H, T, r: int, Q=None, Z=None, stream=None, q: int = 0, chase_ctas: int = 0,
+def ht_stage2(H, T, r: int, Q=None, Z=None, stream=None, q: int = 0,
               validate: bool = True, profile: bool = False, comm=None, root: int = 0,
               emulate_slabs: int = 0):
     """In-place stage two on device tensors (C ABI ``ht_stage2_{d,z}_ex``).
@@ -186,13 +197,17 @@ def ht_stage2(H, T, r: int, Q=None, Z=None, stream=None, q: int = 0, chase_ctas:
     pt, ldt = _check_mat(T, n, "T", dt)
     pq, ldq = _check_mat(Q, n, "Q", dt)
     pz, ldz = _check_mat(Z, n, "Z", dt)
+    for X, nm in ((T, "T"), (Q, "Q"), (Z, "Z")):
+        if X is not None and X.device != H.device:
+            raise ValueError(f"{nm} is on {X.device}, H on {H.device}")
     s = stream if stream is not None else torch.cuda.current_stream(H.device)
-    opts = Opts(q=int(q), chase_ctas=int(chase_ctas), root=int(root),
+    opts = Opts(q=int(q), root=int(root),
                 flags=(0 if validate else 1) | (2 if profile else 0) | (4 if emulate_slabs > 1 else 0))
     opts.reserved[0] = int(emulate_slabs)
     fn = lib.ht_stage2_z_ex if cplx else lib.ht_stage2_d_ex
-    rc = fn(n, int(r), ph, ldh, pt, ldt, pq, ldq, pz, ldz, ctypes.c_void_p(s.cuda_stream),
-            ctypes.c_void_p(comm) if comm else None, ctypes.byref(opts))
+    with torch.cuda.device(H.device):  # the C ABI works on the calling thread's current device
+        rc = fn(n, int(r), ph, ldh, pt, ldt, pq, ldq, pz, ldz, ctypes.c_void_p(s.cuda_stream),
+                ctypes.c_void_p(comm) if comm else None, ctypes.byref(opts))
     if rc != 0:
         raise HTError(rc)
     return H, T, Q, Z
@@ -215,12 +230,18 @@ def ht_stage2_host(H, T, r: int, accumulate: bool = True, q: int = 0, device=Non
         h = torch.from_numpy(np.asfortranarray(A, dtype=np.complex128 if cplx else np.float64))
         return h.t().contiguous().pin_memory().to(dev, non_blocking=True).t()
 
-    Hd, Td = to_dev(H), to_dev(T)
-    Qd = Zd = None
-    if accumulate:
-        Qd = torch.eye(n, dtype=dt, device=dev).t()
-        Zd = torch.eye(n, dtype=dt, device=dev).t()
-    ht_stage2(Hd, Td, r, Qd, Zd, stream=stream, q=q)
+    with torch.cuda.device(dev):
+        Hd, Td = to_dev(H), to_dev(T)
+        Qd = Zd = None
+        if accumulate:
+            Qd = torch.eye(n, dtype=dt, device=dev).t()
+            Zd = torch.eye(n, dtype=dt, device=dev).t()
+        cur = torch.cuda.current_stream(dev)
+        s = stream if stream is not None else cur
+        if s != cur:
+            s.wait_stream(cur)  # the uploads and eye() ran on the current stream
+        ht_stage2(Hd, Td, r, Qd, Zd, stream=s, q=q)
+        s.synchronize()  # the call may return while the reduction still runs on s
 
     def to_host(X):
         return None if X is None else X.t().cpu().numpy().T

@@ -20,6 +20,7 @@ struct AccumArgs {
     const S* Zr;
     S* U;
     S* V;
+    const unsigned long long* gate;  // input-check verdict (input_rejected)
 };
 
 template <typename S>
@@ -30,6 +31,7 @@ __host__ __device__ inline size_t accum_smem_bytes(int r, int qp, bool pre) {
 
 template <typename S, int NT>
 __global__ void __launch_bounds__(NT) accum_kernel(AccumArgs<S> a) {
+    if (input_rejected(a.gate)) return;
     extern __shared__ __align__(16) unsigned char smraw[];
     S* X = reinterpret_cast<S*>(smraw);
     const int n = a.n, r = a.r, qp = a.qp, j1 = a.j1, K = a.K;
@@ -93,6 +95,7 @@ struct MergeArgs {
     const S* V;
     S* MU;       // merged blocks, same layout
     S* MV;
+    const unsigned long long* gate;  // input-check verdict (input_rejected)
 };
 
 template <typename S>
@@ -102,6 +105,7 @@ __host__ __device__ inline size_t merge_smem_bytes(int W, int w) {
 
 template <typename S, int NT>
 __global__ void __launch_bounds__(NT) merge_kernel(MergeArgs<S> a) {
+    if (input_rejected(a.gate)) return;
     extern __shared__ __align__(16) unsigned char smraw[];
     const int n = a.n, r = a.r, qp = a.qp, j1 = a.j1, K = a.K, P = a.P;
     const int mg = blockIdx.x;

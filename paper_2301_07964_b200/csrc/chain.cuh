@@ -51,6 +51,7 @@ struct ChainParams {
     long long* prof;  // optional (HT_K1PROF): cycles by phase of one tile's steps (8 slots)
     int prof_tile;    // the profiled tile of job 0 (HT_CHAIN_PROF_TILE)
     int stair_first;  // right chains: staircase-band tiles dispatched first (HT_STAIR_FIRST=0: off)
+    const unsigned long long* gate;  // input-check verdict (input_rejected)
 };
 
 // H/T chains are latency-bound by their longest tiles (right updates: the top row tiles walk
@@ -596,6 +597,7 @@ __host__ __device__ constexpr int chain_minb() { return (sizeof(S) == 8 && WP <=
 
 template <typename S, int WP>
 __global__ void __launch_bounds__(chain_nt(WP), chain_minb<S, WP>()) chain_kernel(ChainParams<S> P) {
+    if (input_rejected(P.gate)) return;
     extern __shared__ __align__(16) unsigned char smraw[];
     const int total = P.job[0].ntiles + (P.njobs > 1 ? P.job[1].ntiles : 0);
     uint64_t* bars = reinterpret_cast<uint64_t*>(smraw);

@@ -45,6 +45,7 @@ struct ChaseArgs {
     long long* prof;  // optional: per-CTA cycle counts of the step phases (12 slots)
     int prof_t0;      // >= 0: only sweep prof_t0 of each group records
     int hlag;         // helpers take the band rows above b0(k - hlag): 1, or 0 (see far_strip_helper)
+    const unsigned long long* gate;  // input-check verdict (input_rejected)
 };
 
 __device__ __forceinline__ int ld_acquire(const int* p) {
@@ -658,6 +659,7 @@ __device__ __forceinline__ void far_strip_helper(const ChaseArgs<S>& a, int t, i
 
 template <typename S, int NT, int MAXM>
 __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
+    if (input_rejected(a.gate)) return;
     extern __shared__ __align__(16) unsigned char smraw[];
     S* sm = reinterpret_cast<S*>(smraw);
     const int n = a.n, r = a.r, qp = a.qp, j1 = a.j1, K = a.K;

@@ -171,10 +171,11 @@ struct Plan {
     bool qz_late = true;   // Q/Z chains of a group start after its H/T chains (HT_QZ_LATE=0: after K2)
     int hlag = 1;          // helper row split (ChaseArgs::hlag): 0 for r >= 32 (HT_HELPER_LAG overrides)
     size_t mrg_bytes = 0;
+    const unsigned long long* gate = nullptr;  // device verdict words of the input check (nullptr: none)
     bool is_root() const { return comm == nullptr || rank == root; }
     bool qz() const { return Q || Z; }
     bool same(const Plan& o) const {
-        return n == o.n && r == o.r && q == o.q && strip_cap == o.strip_cap && helpers == o.helpers && P == o.P && qz_late == o.qz_late && hlag == o.hlag && H == o.H && ldh == o.ldh &&
+        return n == o.n && r == o.r && q == o.q && strip_cap == o.strip_cap && helpers == o.helpers && P == o.P && qz_late == o.qz_late && hlag == o.hlag && gate == o.gate && H == o.H && ldh == o.ldh &&
                T == o.T && ldt == o.ldt && Q == o.Q && ldq == o.ldq && Z == o.Z && ldz == o.ldz;
     }
 };
@@ -370,7 +371,7 @@ int enqueue_groups(const Plan<S>& p, Workspace<S>& ws, cudaStream_t stream, bool
             ChaseArgs<S> ca{n, r, qp, j1, K, p.H, p.ldh, p.T, p.ldt, ws.Qr, ws.Zr, ws.Tr, TLD, ws.Mg,
                             mcatch_ld(q, r), mcatch_st(q, r), ws.prog, p.strip_cap,
                             p.helpers, ws.k1prof, getenv("HT_K1PROF_T") ? atoi(getenv("HT_K1PROF_T")) : -1,
-                            p.hlag};
+                            p.hlag, p.gate};
             void* kargs[] = {&ca};
             CK(cudaLaunchKernel(p.chase_fn, dim3(qp * (1 + p.helpers)), dim3(CHASE_NT), kargs, p.chase_bytes, stream));
         }
@@ -383,13 +384,13 @@ int enqueue_groups(const Plan<S>& p, Workspace<S>& ws, cudaStream_t stream, bool
         }
         if (qz && g >= NUV) CK(cudaStreamWaitEvent(stream, ws.ev_qz[bsel], 0));  // Q/Z of g-NUV done with U/V[bsel]
         AccumArgs<S> aa{n, r, qp, j1, K, WP, LDB, p.acc_bytes >= accum_smem_bytes<S>(r, q, true) ? 1 : 0, ws.Qr, ws.Zr,
-                        ws.U[bsel], ws.V[bsel]};
+                        ws.U[bsel], ws.V[bsel], p.gate};
         if (root || qz) {
             accum_kernel<S, ACC_NT><<<dim3(K, 2), ACC_NT, p.acc_bytes, stream>>>(aa);
             CK(cudaGetLastError());
             g_last_launches += 2;
             if (p.P > 1) {
-                MergeArgs<S> ma{n, r, qp, j1, K, p.P, WP, LDB, ws.U[bsel], ws.V[bsel], ws.MU[bsel], ws.MV[bsel]};
+                MergeArgs<S> ma{n, r, qp, j1, K, p.P, WP, LDB, ws.U[bsel], ws.V[bsel], ws.MU[bsel], ws.MV[bsel], p.gate};
                 merge_kernel<S, ACC_NT><<<dim3((K + p.P - 1) / p.P, 2), ACC_NT, p.mrg_bytes, stream>>>(ma);
                 CK(cudaGetLastError());
                 ++g_last_launches;
@@ -407,11 +408,13 @@ int enqueue_groups(const Plan<S>& p, Workspace<S>& ws, cudaStream_t stream, bool
                               chain_spread(p.nsm), ws.k1prof ? ws.k1prof + 16 : nullptr,
                               getenv("HT_CHAIN_PROF_TILE") ? atoi(getenv("HT_CHAIN_PROF_TILE")) : 0,
                               !(getenv("HT_STAIR_FIRST") && atoi(getenv("HT_STAIR_FIRST")) == 0)};
+            pr.gate = p.gate;
             if (int rc = chain<S>(pr, WP, 2 * tiles, r, q, stream)) return rc;
             ChainParams<S> pl{n, r, qp, j1, K, {{p.H, p.ldh, ws.U[bsel], ws.MU[bsel], CM_A_LEFT, 1, tiles, 0},
                                                 {p.T, p.ldt, ws.U[bsel], ws.MU[bsel], CM_B_LEFT, 1, tiles, 0}}, 2, ws.Zr, p.P,
                               chain_spread(p.nsm), ws.k1prof ? ws.k1prof + 24 : nullptr,
                               getenv("HT_CHAIN_PROF_TILE") ? atoi(getenv("HT_CHAIN_PROF_TILE")) : 0};
+            pl.gate = p.gate;
             if (int rc = chain<S>(pl, WP, 2 * tiles, r, q, stream)) return rc;
             g_last_launches += 2;
         }
@@ -431,6 +434,7 @@ int enqueue_groups(const Plan<S>& p, Workspace<S>& ws, cudaStream_t stream, bool
                                                      p.Q ? ws.MU[bsel] : ws.MV[bsel], CM_PLAIN, 0, nt, t0},
                                                     {p.Z, p.ldz, ws.V[bsel], ws.MV[bsel], CM_PLAIN, 0, nt, t0}},
                                   (p.Q && p.Z) ? 2 : 1, ws.Zr, p.P};
+                pq.gate = p.gate;
                 // persistent grid leaving q whole SMs: the chase of the next group starts at once
                 if (int rc = chain<S>(pq, WP, std::min(pq.njobs * nt, p.qz_ctas), r, q, ws.side, 116 * 1024)) return rc;
                 ++g_last_launches;
@@ -473,8 +477,32 @@ struct GraphEntry {
 };
 
 template <typename S>
-int graph_for(const Plan<S>& p, cudaStream_t stream, GraphEntry<S>** out) {
+std::vector<GraphEntry<S>*>& graph_cache() {
     static thread_local std::vector<GraphEntry<S>*> cache;
+    return cache;
+}
+
+// Frees every cached graph and its workspace of the calling host thread (ht_release_cache).
+template <typename S>
+int release_graphs() {
+    auto& cache = graph_cache<S>();
+    int rc = HT_OK;
+    int dev0 = 0;
+    CK(cudaGetDevice(&dev0));
+    for (auto* e : cache) {
+        if (cudaSetDevice(e->dev) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) rc = HT_ECUDA;
+        if (e->exec) cudaGraphExecDestroy(e->exec);
+        if (e->ws.release(nullptr, false)) rc = HT_ECUDA;
+        delete e;
+    }
+    cache.clear();
+    CK(cudaSetDevice(dev0));
+    return rc;
+}
+
+template <typename S>
+int graph_for(const Plan<S>& p, cudaStream_t stream, GraphEntry<S>** out) {
+    auto& cache = graph_cache<S>();
     int dev = 0;
     CK(cudaGetDevice(&dev));
     for (auto* e : cache)
@@ -525,6 +553,50 @@ int graph_for(const Plan<S>& p, cudaStream_t stream, GraphEntry<S>** out) {
     return HT_OK;
 }
 
+// Input-check state per (host thread, device): the two verdict words on the device (also the
+// gate every reduction kernel reads), their pinned host copy and the event after the copy.
+struct ValState {
+    unsigned long long* dflags = nullptr;
+    unsigned long long* hflags = nullptr;
+    cudaEvent_t done = nullptr;
+    int dev = -1;
+};
+std::vector<ValState>& val_states() {
+    static thread_local std::vector<ValState> v;
+    return v;
+}
+int val_state(int dev, ValState** out) {
+    auto& v = val_states();
+    for (auto& s : v)
+        if (s.dev == dev) {
+            *out = &s;
+            return HT_OK;
+        }
+    ValState s;
+    s.dev = dev;
+    CK(cudaMalloc(&s.dflags, 2 * sizeof(unsigned long long)));
+    CK(cudaMallocHost(&s.hflags, 2 * sizeof(unsigned long long)));
+    CK(cudaEventCreateWithFlags(&s.done, cudaEventDisableTiming));
+    v.reserve(16);  // (pointers into v stay valid: at most one entry per device)
+    v.push_back(s);
+    *out = &v.back();
+    return HT_OK;
+}
+int release_val_states() {
+    int dev0 = 0;
+    CK(cudaGetDevice(&dev0));
+    for (auto& s : val_states()) {
+        cudaSetDevice(s.dev);
+        cudaEventSynchronize(s.done);
+        cudaEventDestroy(s.done);
+        cudaFree(s.dflags);
+        cudaFreeHost(s.hflags);
+    }
+    val_states().clear();
+    CK(cudaSetDevice(dev0));
+    return HT_OK;
+}
+
 template <typename S>
 int run(int64_t n64, int64_t r64, S* H, int64_t ldh, S* T, int64_t ldt, S* Q, int64_t ldq, S* Z,
         int64_t ldz, cudaStream_t stream, ncclComm_t comm, const ht_opts* opts, bool is_complex) {
@@ -563,23 +635,16 @@ int run(int64_t n64, int64_t r64, S* H, int64_t ldh, S* T, int64_t ldt, S* Q, in
     // The reduction is enqueued right behind the check and the host then waits for the check
     // only: the call returns its verdict while the reduction runs, so back-to-back calls keep
     // the GPU busy (on invalid input the reduction's outputs are undefined, as the header says).
-    struct ValState {
-        unsigned long long* dflags = nullptr;  // device
-        unsigned long long* hflags = nullptr;  // pinned host
-        cudaEvent_t done = nullptr;
-        int dev = -1;
-    };
-    static thread_local ValState vs;
     const bool validate = !(opts && (opts->flags & HT_FLAG_NO_VALIDATE));
+    ValState* vsp = nullptr;
     if (validate) {
         int dev = 0;
         CK(cudaGetDevice(&dev));
-        if (vs.dev != dev) {  // (per host thread and device; the old device's state is dropped)
-            CK(cudaMalloc(&vs.dflags, 2 * sizeof(unsigned long long)));
-            CK(cudaMallocHost(&vs.hflags, 2 * sizeof(unsigned long long)));
-            CK(cudaEventCreateWithFlags(&vs.done, cudaEventDisableTiming));
-            vs.dev = dev;
-        }
+        if (int rv = val_state(dev, &vsp)) return rv;
+    }
+    static ValState no_check;  // (validate == false: never read)
+    ValState& vs = vsp ? *vsp : no_check;
+    if (validate) {
         CK(cudaMemsetAsync(vs.dflags, 0, 2 * sizeof(unsigned long long), stream));
         validate_kernel<S><<<4 * 148, 256, 0, stream>>>(n, r, H, ldh, T, ldt, Q, ldq, Z, ldz, vs.dflags);
         ++g_last_launches;
@@ -593,6 +658,12 @@ int run(int64_t n64, int64_t r64, S* H, int64_t ldh, S* T, int64_t ldt, S* Q, in
         if (vs.hflags[0]) return HT_ESTRUCT;
         if (vs.hflags[1]) return HT_ENONFINITE;
         return HT_OK;
+    };
+    // an error after the check was enqueued: wait for the check's copy before returning, so that
+    // the next call does not reset the verdict words while this one may still read them
+    auto fail = [&](int code) -> int {
+        if (validate) cudaEventSynchronize(vs.done);
+        return code;
     };
     if (n <= 2 || r <= 1) return verdict();  // exact no-op
     // a call refused before any launch still reports an input error first
@@ -658,6 +729,7 @@ int run(int64_t n64, int64_t r64, S* H, int64_t ldh, S* T, int64_t ldt, S* Q, in
     // (measured: configs 2 / 3 / 4 -0.8 / -0.3 / -1.1 % per step; HT_QZ_LATE=0 restores the early start)
     pl.qz_late = !(getenv("HT_QZ_LATE") && atoi(getenv("HT_QZ_LATE")) == 0);
     pl.mrg_bytes = mrg_bytes;
+    pl.gate = validate ? vs.dflags : nullptr;
     if (comm) {
         pl.comm = comm;
         NK(ncclCommCount(comm, &pl.nranks));
@@ -672,17 +744,17 @@ int run(int64_t n64, int64_t r64, S* H, int64_t ldh, S* T, int64_t ldt, S* Q, in
     if (prof || k1p || comm || getenv("HT_NO_GRAPH")) {
         // direct launches (per-kernel-class events / K1 phase counters need them)
         Workspace<S> ws;
-        if ((rc = ws.alloc(pl, stream, /*async=*/true, k1p))) return rc;
+        if ((rc = ws.alloc(pl, stream, /*async=*/true, k1p))) return fail(rc);
         rc = enqueue_groups<S>(pl, ws, stream, prof);
         if (int rf = ws.release(stream, /*async=*/true)) rc = rc ? rc : rf;
-        if (rc) return rc;
+        if (rc) return fail(rc);
         if (int rv = verdict()) return rv;
         if (k1p) print_k1prof(ws.k1prof_host);
     } else {
         // the whole group loop as one cached CUDA graph (one launch per call; no host stalls)
         GraphEntry<S>* ge = nullptr;
-        if ((rc = graph_for<S>(pl, stream, &ge))) return rc;
-        CK(cudaGraphLaunch(ge->exec, stream));
+        if ((rc = graph_for<S>(pl, stream, &ge))) return fail(rc);
+        if (cudaGraphLaunch(ge->exec, stream) != cudaSuccess) return fail(HT_ECUDA);
         g_last_launches += ge->launches;
         if (int rv = verdict()) return rv;
     }
@@ -758,6 +830,13 @@ int ht_slab_range(int64_t n, int nranks, int rank, int64_t* row0, int64_t* nrows
     *row0 = std::min<int64_t>(a, n);
     *nrows = std::max<int64_t>(0, std::min<int64_t>(n, (int64_t)(t0 + nt) * CH_BM) - *row0);
     return HT_OK;
+}
+
+int ht_release_cache(void) {
+    int rc = release_graphs<double>();
+    if (int r2 = release_graphs<zc>()) rc = rc ? rc : r2;
+    if (int r3 = release_val_states()) rc = rc ? rc : r3;
+    return rc;
 }
 
 int ht_comm_destroy(ncclComm_t comm) {

@@ -1,4 +1,4 @@
-// misc.cuh -- K5 utilities: input validation, workspace initialisation, DMMA probe.
+// misc.cuh -- K5 utilities: input validation, slab (un)packing, DMMA / DFMA peak probes.
 #pragma once
 #include "scalar.cuh"
 
@@ -23,24 +23,6 @@ __global__ void validate_kernel(int n, int r, const S* H, int64_t ldh, const S* 
     }
     if (bad_struct) atomicAdd(&flags[0], bad_struct);
     if (bad_fin) atomicAdd(&flags[1], bad_fin);
-}
-
-// U_k = V_k = I_{w_k} for the K windows of a group (row-major WP x LDB blocks; all
-// other entries zero so padded K rows contribute nothing in the DMMA chains).
-template <typename S>
-__global__ void init_blocks_kernel(S* U, S* V, int K, int WP, int LDB, int n, int j1, int w, int r) {
-    const int64_t per = (int64_t)WP * LDB;
-    const int64_t total = per * K;
-    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
-         e += (int64_t)gridDim.x * blockDim.x) {
-        const int k = (int)(e / per);
-        const int64_t x = e % per;
-        const int l = (int)(x / LDB), c = (int)(x % LDB);
-        const int wk = min(w, n - (j1 + k * r + 1) + 1);
-        const S val = S((l == c && l < wk) ? 1.0 : 0.0);
-        U[e] = val;
-        V[e] = val;
-    }
 }
 
 // ---------------------------------------------------------------------------------------

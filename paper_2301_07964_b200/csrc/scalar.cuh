@@ -102,3 +102,11 @@ __device__ __forceinline__ double fast_rsqrt(double x) {
     e = fma(-h, y, 1.0);
     return fma(0.5 * e, y, y);
 }
+
+// Input-check gate (a rejected input is left untouched): every kernel of the
+// reduction reads the two verdict words K5 wrote just before it on the stream and returns at
+// once if either is set.  gate == nullptr: no check was requested.
+__device__ __forceinline__ bool input_rejected(const unsigned long long* gate) {
+    if (!gate) return false;
+    return (__ldcg(gate) | __ldcg(gate + 1)) != 0ull;
+}

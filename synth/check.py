@@ -42,16 +42,23 @@ def phase_factors(H, T):
     dq_{i+1} = H_{i+1,i} dz_i / |H_{i+1,i} dz_i|.  Zero entries keep d = 1."""
     H = np.asarray(H)
     T = np.asarray(T)
-    n = H.shape[0]
-    cplx = np.iscomplexobj(H) or np.iscomplexobj(T)
+    return phase_factors_diag(np.diagonal(H, -1), np.diagonal(T))
+
+
+def phase_factors_diag(hsub, tdiag):
+    """phase_factors from H's first subdiagonal (n-1) and T's diagonal (n) alone."""
+    hsub = np.asarray(hsub)
+    tdiag = np.asarray(tdiag)
+    n = tdiag.shape[0]
+    cplx = np.iscomplexobj(hsub) or np.iscomplexobj(tdiag)
     dt = np.complex128 if cplx else np.float64
     dq = np.ones(n, dt)
     dz = np.ones(n, dt)
     for i in range(n):
-        if i >= 1 and T[i, i] != 0:
-            dz[i] = dq[i] * abs(T[i, i]) / T[i, i]
-        if i < n - 1 and H[i + 1, i] != 0:
-            h = H[i + 1, i] * dz[i]
+        if i >= 1 and tdiag[i] != 0:
+            dz[i] = dq[i] * abs(tdiag[i]) / tdiag[i]
+        if i < n - 1 and hsub[i] != 0:
+            h = hsub[i] * dz[i]
             dq[i + 1] = h / abs(h)
     return dq, dz
 
@@ -76,3 +83,30 @@ def forward_gap(H1, T1, H2, T2):
     a = normalize_phase(H1, T1)
     b = normalize_phase(H2, T2)
     return max(rel_diff(a[0], b[0]), rel_diff(a[1], b[1]))
+
+
+def normalise_samples(raw: dict, dq, dz, cols, rows) -> dict:
+    """Reading c10 applied to sampled columns / rows only (full-size comparisons).
+
+    raw[name] = (X[:, cols], X[rows, :]) for name in H, T, Q, Z (raw, un-normalised);
+    returns {name_cols, name_rows} of H' = D_Q^* H D_Z, T' = D_Q^* T D_Z, Q' = Q D_Q, Z' = Z D_Z."""
+    cols = np.asarray(cols)
+    rows = np.asarray(rows)
+    out = {}
+    for nm, dl, dr in (("H", dq, dz), ("T", dq, dz), ("Q", None, dq), ("Z", None, dz)):
+        c, rr = raw[nm]
+        c = np.asarray(c) * dr[cols][None, :]
+        rr = np.asarray(rr) * dr[None, :]
+        if dl is not None:
+            c = dl.conj()[:, None] * c
+            rr = dl.conj()[rows][:, None] * rr
+        out[nm + "_cols"] = c
+        out[nm + "_rows"] = rr
+    return out
+
+
+def sample_rel_diff(a: dict, b: dict, nm: str) -> float:
+    """Relative Frobenius difference of the sampled entries of matrix nm (b is the reference)."""
+    num = np.linalg.norm(a[nm + "_cols"] - b[nm + "_cols"]) ** 2 + np.linalg.norm(a[nm + "_rows"] - b[nm + "_rows"]) ** 2
+    den = np.linalg.norm(b[nm + "_cols"]) ** 2 + np.linalg.norm(b[nm + "_rows"]) ** 2
+    return float(np.sqrt(num / max(den, 1e-300)))

@@ -32,7 +32,7 @@ def _host(X):
     return X.cpu().numpy()
 
 
-def run_gpu(H, T, r, q=0, accumulate=True, chase_ctas=0, Qin=None, Zin=None):
+def run_gpu(H, T, r, q=0, accumulate=True, Qin=None, Zin=None):
     ht = _ht()
     n = H.shape[0]
     Hd, Td = _dev(H), _dev(T)
@@ -41,7 +41,7 @@ def run_gpu(H, T, r, q=0, accumulate=True, chase_ctas=0, Qin=None, Zin=None):
     if accumulate:
         Qd = _dev(np.eye(n, dtype=H.dtype) if Qin is None else Qin)
         Zd = _dev(np.eye(n, dtype=H.dtype) if Zin is None else Zin)
-    ht.ht_stage2(Hd, Td, r, Qd, Zd, q=q, chase_ctas=chase_ctas)
+    ht.ht_stage2(Hd, Td, r, Qd, Zd, q=q)
     torch.cuda.synchronize()
     return _host(Hd), _host(Td), None if Qd is None else _host(Qd), None if Zd is None else _host(Zd)
 
@@ -144,12 +144,18 @@ def test_no_accumulation_bitwise_same_HT():
     assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
 
 
-def test_deterministic_and_wavefront_width_independent():
-    # lag-3 wavefront: any number of chase CTAs gives bitwise the same result [V11]
+def test_deterministic_repeated_calls():
+    # the lag-3 wavefront's inter-CTA ordering fixes every reflector's inputs (SURVEY A.4 [V11]):
+    # repeated calls -- graph replays and a direct-launch call -- are bitwise identical
+    import os
     H, T = make_pencil(300, 10, seed=7)
-    a = run_gpu(H, T, 10, q=12, chase_ctas=1)
-    b = run_gpu(H, T, 10, q=12, chase_ctas=12)
-    c = run_gpu(H, T, 10, q=12, chase_ctas=4)
+    a = run_gpu(H, T, 10, q=12)
+    b = run_gpu(H, T, 10, q=12)
+    os.environ["HT_NO_GRAPH"] = "1"
+    try:
+        c = run_gpu(H, T, 10, q=12)
+    finally:
+        os.environ.pop("HT_NO_GRAPH", None)
     for x, y, z in zip(a, b, c):
         assert np.array_equal(x, y) and np.array_equal(x, z)
 
@@ -188,9 +194,53 @@ def test_error_codes():
     with pytest.raises(ht.HTError) as e:
         ht.ht_stage2(Hd, _dev(T), -1)
     assert e.value.code == -2
-    # the rejected calls' reductions were enqueued behind the check (header: outputs undefined);
-    # they must leave the library in a state where the next valid call is exact
     check_parity(H, T, 4)
+
+
+@pytest.mark.parametrize("graph", [True, False])
+def test_rejected_input_left_untouched(graph):
+    # the check runs before any work -- every reduction kernel reads the device
+    # verdict and exits, so on return codes 1 / 2 the caller's buffers are unchanged
+    import os
+    ht = _ht()
+    n, r = 130, 6
+    H, T = make_pencil(n, r, seed=19)
+    Hb = H.copy(order="F")
+    Hb[n - 1, 3] = 1e-200  # roundoff below the r-th subdiagonal
+    Tn = T.copy(order="F")
+    Tn[7, 9] = np.inf
+    if not graph:
+        os.environ["HT_NO_GRAPH"] = "1"
+    try:
+        for (h0, t0, code) in ((Hb, T, 1), (H, Tn, 2)):
+            Hd, Td = _dev(h0), _dev(t0)
+            Qd, Zd = _dev(np.eye(n)), _dev(np.eye(n))
+            with pytest.raises(ht.HTError) as e:
+                ht.ht_stage2(Hd, Td, r, Qd, Zd)
+            assert e.value.code == code
+            torch.cuda.synchronize()
+            assert np.array_equal(_host(Hd), h0) and np.array_equal(_host(Td), t0)
+            assert np.array_equal(_host(Qd), np.eye(n)) and np.array_equal(_host(Zd), np.eye(n))
+            # the caller cleans the input and retries on the same buffers
+            if code == 1:
+                Hd[n - 1, 3] = 0.0
+                ht.ht_stage2(Hd, Td, r, Qd, Zd)
+                torch.cuda.synchronize()
+                inv = invariants(H, T, _host(Hd), _host(Td), _host(Qd), _host(Zd))
+                assert max(inv["eA"], inv["eB"], inv["oQ"], inv["oZ"]) <= inv["bound"]
+    finally:
+        os.environ.pop("HT_NO_GRAPH", None)
+
+
+def test_release_cache_then_call_again():
+    ht = _ht()
+    H, T = make_pencil(150, 7, seed=23)
+    a = run_gpu(H, T, 7)
+    ht.release_cache()
+    ht.release_cache()  # idempotent
+    b = run_gpu(H, T, 7)
+    for x, y in zip(a, b):
+        assert np.array_equal(x, y)
 
 
 # ---------------------------------------------------------------------------- multi-GPU decomposition

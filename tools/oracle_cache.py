@@ -32,7 +32,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 import oracle  # noqa: E402
-from synth.check import U, phase_factors, structure_violations  # noqa: E402
+from synth.check import U, normalise_samples, phase_factors, sample_rel_diff, structure_violations  # noqa: E402
 from synth.pencil import CONFIGS, config_pencil  # noqa: E402
 
 
@@ -44,23 +44,8 @@ def sample_indices(n: int, k: int, seed: int):
 
 def normalised_samples(H, T, Q, Z, cols, rows):
     dq, dz = phase_factors(H, T)
-    out = {}
-    for nm, X, dl, dr in (("H", H, dq, dz), ("T", T, dq, dz), ("Q", Q, None, dq), ("Z", Z, None, dz)):
-        # H' = D_Q^* H D_Z, T' likewise; Q' = Q D_Q, Z' = Z D_Z  (reading c10)
-        c = X[:, cols] * dr[cols][None, :]
-        rr = X[rows, :] * dr[None, :]
-        if dl is not None:
-            c = dl.conj()[:, None] * c
-            rr = dl.conj()[rows][:, None] * rr
-        out[nm + "_cols"] = c
-        out[nm + "_rows"] = rr
-    return out
-
-
-def sample_rel(a: dict, b: dict, nm: str) -> float:
-    num = np.linalg.norm(a[nm + "_cols"] - b[nm + "_cols"]) ** 2 + np.linalg.norm(a[nm + "_rows"] - b[nm + "_rows"]) ** 2
-    den = np.linalg.norm(b[nm + "_cols"]) ** 2 + np.linalg.norm(b[nm + "_rows"]) ** 2
-    return float(np.sqrt(num / max(den, 1e-300)))
+    raw = {nm: (X[:, cols], X[rows, :]) for nm, X in (("H", H), ("T", T), ("Q", Q), ("Z", Z))}
+    return normalise_samples(raw, dq, dz, cols, rows)
 
 
 def invariants_blas(A, B, H, T, Q, Z):
@@ -112,7 +97,7 @@ def main():
         del Hp, Tp
         fp = normalised_samples(hp, tp, qp, zp, cols, rows)
         del hp, tp, qp, zp
-        meta["floor"] = {nm: sample_rel(fp, res, nm) for nm in "HTQZ"}
+        meta["floor"] = {nm: sample_rel_diff(fp, res, nm) for nm in "HTQZ"}
         print("noise floor (oracle vs oracle on u-perturbed input, sampled rel. diff)", meta["floor"], flush=True)
     os.makedirs(args.out, exist_ok=True)
     fn = os.path.join(args.out, f"cfg{args.cfg}" + (f"_n{n}" if args.n else "") + ".npz")
