@@ -18,6 +18,7 @@
 // into the dense window blocks U_k, V_k for the apply phase.
 #pragma once
 #include "scalar.cuh"
+#include "rqw.cuh"
 
 #ifndef IDX
 #define IDX(p, ld, i, j) (p)[((int64_t)(i) - 1) + ((int64_t)(j) - 1) * (int64_t)(ld)]
@@ -500,11 +501,27 @@ __device__ __forceinline__ void rq_direction_u(int m, const S* Cb, int LDC, S* r
 template <typename S, int MAXM>
 __host__ __device__ constexpr bool rq_unrolled() { return MAXM * (int)sizeof(S) <= 256; }  // real <= 32, complex <= 16
 template <typename S, int MAXM>
-__host__ __device__ constexpr int rq_nthr() { return rq_unrolled<S, MAXM>() ? 64 : RQCfg<S, MAXM>::NTHR; }
+__host__ __device__ constexpr bool rq_warp_rows();
+template <typename S, int MAXM>
+__host__ __device__ constexpr int rq_nthr() {
+    return rq_unrolled<S, MAXM>() ? 64 : (rq_warp_rows<S, MAXM>() ? 256 : RQCfg<S, MAXM>::NTHR);
+}
+
+// real m > 32: the warp-row RQ of rqw.cuh (8 warps; the ring is its work storage, ld ring_pld)
+template <typename S, int MAXM>
+__host__ __device__ constexpr bool rq_warp_rows() {
+#ifdef HT_RQW_OFF
+    return false;
+#else
+    return sizeof(S) == 8 && MAXM >= 64;
+#endif
+}
 
 template <typename S, int MAXM>
-__device__ __forceinline__ void rq_dir(int m, const S* Cb, int LDC, S* ring, volatile int* flag, S* uu) {
+__device__ __forceinline__ void rq_dir(int m, const S* Cb, int LDC, S* ring, volatile int* flag, S* uu,
+                                       int ring_ld = 0) {
     if constexpr (rq_unrolled<S, MAXM>()) rq_direction_u<S, MAXM>(m, Cb, LDC, ring, flag, uu);
+    else if constexpr (rq_warp_rows<S, MAXM>()) rq_direction_w<S, MAXM, 8>(m, Cb, LDC, ring, ring_ld, flag, uu);
     else rq_direction<S, MAXM>(m, Cb, LDC, ring, flag, uu);
 }
 
@@ -1168,7 +1185,7 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
                         }
                     }
                 }
-                if (tid < rq_nthr<S, MAXM>()) rq_dir<S, MAXM>(m, Cb, LDC, ring, &rq_flag, uu);
+                if (tid < rq_nthr<S, MAXM>()) rq_dir<S, MAXM>(m, Cb, LDC, ring, &rq_flag, uu, OVERLAY ? 132 : ring_pld(r));
                 if (pf_next) k1_wait_group<1>();  // the strip (the prefetch group may stay in flight)
                 else k1_wait_group<0>();
                 __syncthreads();
