@@ -507,21 +507,24 @@ __host__ __device__ constexpr int rq_nthr() {
     return rq_unrolled<S, MAXM>() ? 64 : (rq_warp_rows<S, MAXM>() ? 256 : RQCfg<S, MAXM>::NTHR);
 }
 
-// real m > 32: the warp-row RQ of rqw.cuh (8 warps; the ring is its work storage, ld ring_pld)
+// real 64 < m <= 128: the warp-row RQ of rqw.cuh (8 warps; the ring is its work storage, ld 132).
+// Measured per RQ of a 128 x 128 block: 313k cycles alone / 444k inside the chase kernel against
+// ~1M for rq_direction; at m = 64 (90k alone) it lost inside the chase kernel (103k RQ, slower
+// other phases: register pressure) to rq_direction (~100k), which therefore stays for r <= 64.
 template <typename S, int MAXM>
 __host__ __device__ constexpr bool rq_warp_rows() {
 #ifdef HT_RQW_OFF
     return false;
 #else
-    return sizeof(S) == 8 && MAXM >= 64;
+    return sizeof(S) == 8 && MAXM >= 128;
 #endif
 }
 
 template <typename S, int MAXM>
 __device__ __forceinline__ void rq_dir(int m, const S* Cb, int LDC, S* ring, volatile int* flag, S* uu,
-                                       int ring_ld = 0) {
+                                       int ring_ld = 0, uint64_t* bars = nullptr, int par = 0) {
     if constexpr (rq_unrolled<S, MAXM>()) rq_direction_u<S, MAXM>(m, Cb, LDC, ring, flag, uu);
-    else if constexpr (rq_warp_rows<S, MAXM>()) rq_direction_w<S, MAXM, 8>(m, Cb, LDC, ring, ring_ld, flag, uu);
+    else if constexpr (rq_warp_rows<S, MAXM>()) rq_direction_w<S, MAXM, 8>(m, Cb, LDC, ring, ring_ld, bars, par, uu);
     else rq_direction<S, MAXM>(m, Cb, LDC, ring, flag, uu);
 }
 
@@ -701,6 +704,11 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
     S* scal = uu + (r + 8) + (OVERLAY ? 0 : (size_t)r * ring_pld(r));
     __shared__ int rq_flag;
     if (threadIdx.x == 0) rq_flag = 1 << 30;
+    // warp-row RQ (rqw.cuh): one mbarrier per stage, one phase per RQ call
+    constexpr bool RQW_ON = rq_warp_rows<S, MAXM>();
+    __shared__ uint64_t rq_bars[RQW_ON ? MAXM : 1];
+    if (RQW_ON && threadIdx.x < 32) rqw_bars_init(rq_bars, MAXM);
+    int rq_calls = 0;
     S* rec0 = scal + 16;       // qp x (r+1): v of Q_k^{j1+s}, tau at [r]
     S* Tsm0 = rec0 + (size_t)qp * (r + 1);  // T(p, s) at Tsm[p*TL + s]
     S* wx = Tsm0 + (size_t)qp * TL;       // Y^* x, then T^* Y^* x
@@ -1185,7 +1193,9 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
                         }
                     }
                 }
-                if (tid < rq_nthr<S, MAXM>()) rq_dir<S, MAXM>(m, Cb, LDC, ring, &rq_flag, uu, OVERLAY ? 132 : ring_pld(r));
+                if (tid < rq_nthr<S, MAXM>())
+                    rq_dir<S, MAXM>(m, Cb, LDC, ring, &rq_flag, uu, OVERLAY ? 132 : ring_pld(r), rq_bars, rq_calls & 1);
+                ++rq_calls;
                 if (pf_next) k1_wait_group<1>();  // the strip (the prefetch group may stay in flight)
                 else k1_wait_group<0>();
                 __syncthreads();

@@ -6,6 +6,9 @@
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
+#ifndef REPS
+#define REPS 10
+#endif
 
 #include "../paper_2301_07964_b200/csrc/chase.cuh"
 #include "../paper_2301_07964_b200/csrc/rqw.cuh"
@@ -14,10 +17,13 @@ template <int MAXM, bool NEW>
 __global__ void run(const double* C0, double* out, long long* cyc, int m, int reps) {
     extern __shared__ double dyn[];
     const int LDC = MAXM + 1, HLD = MAXM + 4;
-    double* Cb = dyn;
-    double* hb = Cb + MAXM * LDC;
+    double* Cb = dyn;  // (MAXM = 128: the work rows overlay the block, as in the chase kernel)
+    double* hb = MAXM > 64 ? Cb : Cb + MAXM * LDC;
     double* uu = hb + MAXM * HLD;
     __shared__ int flag;
+    __shared__ uint64_t bars[128];
+    if (threadIdx.x < 32) rqw_bars_init(bars, 128);
+    __syncthreads();
     long long tot = 0;
     for (int it = 0; it < reps; ++it) {
         for (int e = threadIdx.x; e < m * m; e += blockDim.x) Cb[(e % m) + (e / m) * LDC] = C0[e];
@@ -25,9 +31,9 @@ __global__ void run(const double* C0, double* out, long long* cyc, int m, int re
         __syncthreads();
         long long t0 = clock64();
         if constexpr (NEW) {
-            rq_direction_w<double, MAXM, 8>(m, Cb, LDC, hb, HLD, &flag, uu);
+            rq_direction_w<double, MAXM, 8>(m, Cb, LDC, hb, HLD, bars, it & 1, uu);
         } else {
-            if (threadIdx.x < rq_nthr<double, MAXM>()) rq_dir<double, MAXM>(m, Cb, LDC, hb, &flag, uu);
+            if (threadIdx.x < RQCfg<double, MAXM>::NTHR) rq_direction<double, MAXM>(m, Cb, LDC, hb, &flag, uu);
         }
         __syncthreads();
         tot += clock64() - t0;
@@ -38,9 +44,9 @@ __global__ void run(const double* C0, double* out, long long* cyc, int m, int re
 
 template <int MAXM, bool NEW>
 void launch(const double* C, double* out, long long* cyc, int m, int reps) {
-    const int bytes = (MAXM * (MAXM + 1) + MAXM * (MAXM + 4) + MAXM + 8) * 8;
+    const int bytes = ((MAXM > 64 ? 0 : MAXM * (MAXM + 1)) + MAXM * (MAXM + 4) + MAXM + 8) * 8;
     cudaFuncSetAttribute(run<MAXM, NEW>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-    const int nt = NEW ? 256 : (rq_nthr<double, MAXM>() > 256 ? rq_nthr<double, MAXM>() : 256);
+    const int nt = NEW ? 256 : (RQCfg<double, MAXM>::NTHR > 256 ? RQCfg<double, MAXM>::NTHR : 256);
     run<MAXM, NEW><<<1, nt, bytes>>>(C, out, cyc, m, reps);
 }
 
@@ -73,10 +79,10 @@ int main() {
                     if (i == j && j % 5 == 2) C[i + j * m] = 0.0;
                 }
         if (cs.maxm == 64) {
-            launch<64, true>(C, o1, c1, m, 10);
+            launch<64, true>(C, o1, c1, m, REPS);
             launch<64, false>(C, o2, c2, m, 10);
         } else {
-            launch<128, true>(C, o1, c1, m, 10);
+            launch<128, true>(C, o1, c1, m, REPS);
             launch<128, false>(C, o2, c2, m, 10);
         }
         cudaError_t err = cudaDeviceSynchronize();
