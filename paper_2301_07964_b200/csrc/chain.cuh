@@ -185,7 +185,7 @@ __device__ __forceinline__ S maybe_conj(S x, bool c) {
 // One tile's descending-k chain.  Returns true if it initialised (and so must invalidate) the
 // ring's mbarriers.
 template <typename S, int WP>
-__device__ __forceinline__ bool chain_tile(const ChainParams<S>& P, int bid, unsigned char* smraw) {
+__device__ __forceinline__ bool chain_tile(const ChainParams<S>& P, int bid, unsigned char* smraw, int grp, int gbar) {
     constexpr int LDB = chain_ldb(WP);
     constexpr int CH_NT = chain_nt(WP);
     constexpr int NW = CH_NT / 32;
@@ -241,8 +241,11 @@ __device__ __forceinline__ bool chain_tile(const ChainParams<S>& P, int bid, uns
         while (kstart >= 0 && cstart(kstart) >= R1) --kstart;
         if (kstart < 0) return false;
     }
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int tid = threadIdx.x - grp * CH_NT, lane = tid & 31, warp = tid >> 5;  // (within the group)
     const int wn = warp % WN, wm = warp / WN;
+    // gbar: barrier of this tile group (chain_kernel2: group g uses bar g + 1; chain_kernel: the CTA
+    // barrier 0)
+    auto gsync = [&]() { asm volatile("bar.sync %0, %1;" ::"r"(gbar), "r"(CH_NT) : "memory"); };
     // ---- step sequence: from window khi downward, a step covers windows [klo, khi]: a whole
     // merge group [mg P, mg P + P - 1] when khi is its top and the tile is fully inside every
     // window of it (no staircase / column limit), else the single window khi ----
@@ -266,7 +269,7 @@ __device__ __forceinline__ bool chain_tile(const ChainParams<S>& P, int bid, uns
         for (int s = 0; s < CH_STAGES; ++s) mbar_init(&bars[s], 1);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
-    __syncthreads();
+    gsync();
 
     // global element access (1-based tile row g, chain index c)
     auto gptr = [&](int g, int c) -> S* {
@@ -356,7 +359,7 @@ __device__ __forceinline__ bool chain_tile(const ChainParams<S>& P, int bid, uns
         const int shift = has_next ? (klo - nklo) * r : 0;  // fresh columns of the next step
         const int cn = has_next ? min(qp - 1, wk) : 0;      // carried into the next step
         cp_async_wait_all();
-        __syncthreads();
+        gsync();
         // prefetch: fresh columns of the next step and (H/T right) this window's staircase reflectors
         if (has_next) {
             int pn = p - shift;
@@ -386,7 +389,7 @@ __device__ __forceinline__ bool chain_tile(const ChainParams<S>& P, int bid, uns
         for (int ch = 0; ch < nch; ++ch) {
             const int s = cseq % CH_STAGES;
             mbar_wait(&bars[s], (cseq / CH_STAGES) & 1);
-            __syncthreads();  // everyone is past chunk cseq-1: its stage may be refilled
+            gsync();  // everyone is past chunk cseq-1: its stage may be refilled
             issue_next();
             const S* Bs = ring + (size_t)s * CH_KC * LDB;
             if (wn * (WP / WN) < wk) {  // warp-uniform: this warp's columns exist in the step
@@ -414,7 +417,7 @@ __device__ __forceinline__ bool chain_tile(const ChainParams<S>& P, int bid, uns
             }
             ++cseq;
         }
-        __syncthreads();  // all reads of X done
+        gsync();  // all reads of X done
         tick(1);
         // ---- epilogue: write Y back in place for the rows the mode updates ----
         const int ylo = (!merged && (mode == CM_A_LEFT || mode == CM_B_LEFT)) ? cstart(k) : 0;
@@ -444,7 +447,7 @@ __device__ __forceinline__ bool chain_tile(const ChainParams<S>& P, int bid, uns
             // reflectors t with g <= i4a(t) (a suffix); zeroing the dots outside it and the upper
             // triangular T keep exactly that suffix.  Steps without a reflector have a zero record.
             cp_async_wait_all();
-            __syncthreads();
+            gsync();
             tick(2);  // (profile: the wait for the staircase data counts as epilogue)
             constexpr int TPR = CH_NT / CH_BM, BZ = CH_SBZ;  // threads per row, reflectors per block
             const int row = tid / TPR, part = tid % TPR;
@@ -471,7 +474,7 @@ __device__ __forceinline__ bool chain_tile(const ChainParams<S>& P, int bid, uns
                 }
                 Gs[e] = gg;
             }
-            __syncthreads();
+            gsync();
             // block factor (xLARFT forward): T(i,i) = sigma_i, T(i,j) = -sigma_j sum_l T(i,l) G(l,j)
             // rows of T are independent given G: T(i,j) = -sigma_j sum_{l=i}^{j-1} T(i,l) G(l,j),
             // so one thread per (block, row) runs along its row
@@ -498,7 +501,7 @@ __device__ __forceinline__ bool chain_tile(const ChainParams<S>& P, int bid, uns
                     Tr[jj] = v;
                 }
             }
-            __syncthreads();
+            gsync();
             tick(0);  // (profile: the block factors count as wait+prefetch)
             // block rounds, with compile-time trip counts (MR >= r): no loop branches in the chain
             auto rounds = [&](auto mrc) {
@@ -564,7 +567,7 @@ __device__ __forceinline__ bool chain_tile(const ChainParams<S>& P, int bid, uns
             else if (r <= 64) rounds(std::integral_constant<int, 64>{});
             else rounds(std::integral_constant<int, 128>{});
         }
-        __syncthreads();
+        gsync();
         tick(3);
         // columns [cn, wk) are final for this group; [0, cn) stay as window k-1's carry
         {
@@ -602,7 +605,7 @@ __global__ void __launch_bounds__(chain_nt(WP), chain_minb<S, WP>()) chain_kerne
     const int total = P.job[0].ntiles + (P.njobs > 1 ? P.job[1].ntiles : 0);
     uint64_t* bars = reinterpret_cast<uint64_t*>(smraw);
     for (int b = blockIdx.x; b < total; b += gridDim.x) {
-        const bool used = chain_tile<S, WP>(P, b, smraw);
+        const bool used = chain_tile<S, WP>(P, b, smraw, 0, 0);
         __syncthreads();
         if (used && threadIdx.x == 0)
             for (int s = 0; s < CH_STAGES; ++s)
@@ -611,3 +614,25 @@ __global__ void __launch_bounds__(chain_nt(WP), chain_minb<S, WP>()) chain_kerne
     }
 }
 
+// Two tile groups per CTA (2 x CH_NT threads, 2 x the shared memory of chain_kernel): group g walks
+// tiles 2 b + g.  For the side-stream Q/Z chains, which must keep to one CTA per SM (the rest of the
+// SMs belong to the next chase): the groups' steps interleave, so one group's epilogue, stores and
+// barriers overlap the other group's DMMA stream (named barriers per group).
+template <typename S, int WP>
+__global__ void __launch_bounds__(2 * chain_nt(WP), 1) chain_kernel2(ChainParams<S> P, unsigned grp_bytes) {
+    if (input_rejected(P.gate)) return;
+    extern __shared__ __align__(16) unsigned char smraw[];
+    constexpr int NT = chain_nt(WP);
+    const int grp = threadIdx.x / NT;
+    unsigned char* sm = smraw + (size_t)grp * grp_bytes;
+    const int total = P.job[0].ntiles + (P.njobs > 1 ? P.job[1].ntiles : 0);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sm);
+    for (int b = 2 * blockIdx.x + grp; b < total; b += 2 * gridDim.x) {
+        const bool used = chain_tile<S, WP>(P, b, sm, grp, 1 + grp);
+        asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(NT) : "memory");
+        if (used && threadIdx.x == grp * NT)
+            for (int s = 0; s < CH_STAGES; ++s)
+                asm volatile("mbarrier.inval.shared::cta.b64 [%0];\n" ::"r"(smem_u32(&bars[s])) : "memory");
+        asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(NT) : "memory");
+    }
+}

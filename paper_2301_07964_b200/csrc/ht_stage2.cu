@@ -82,18 +82,50 @@ int chain(const ChainParams<S>& P, int WP, int grid, int r, int q, cudaStream_t 
     }
 }
 
+// Q/Z chains as two tile groups per CTA (chain_kernel2): one CTA per SM, 2 x the group bytes
+template <typename S, int WP>
+int launch_chain2(const ChainParams<S>& P, int grid, int r, int q, cudaStream_t st) {
+    const size_t gb = (chain_bytes<S, WP>(r, q, P.P) + 127) / 128 * 128;
+    static bool attr_set = false;
+    if (!attr_set) {
+        CK(cudaFuncSetAttribute(chain_kernel2<S, WP>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        attr_set = true;
+    }
+    chain_kernel2<S, WP><<<grid, 2 * chain_nt(WP), 2 * gb, st>>>(P, (unsigned)gb);
+    CK(cudaGetLastError());
+    return HT_OK;
+}
+
+template <typename S>
+int chain2(const ChainParams<S>& P, int WP, int grid, int r, int q, cudaStream_t st) {
+    switch (WP) {
+        case 32: return launch_chain2<S, 32>(P, grid, r, q, st);
+        case 64: return launch_chain2<S, 64>(P, grid, r, q, st);
+        case 96: return launch_chain2<S, 96>(P, grid, r, q, st);
+        case 128: return launch_chain2<S, 128>(P, grid, r, q, st);
+        case 160: return launch_chain2<S, 160>(P, grid, r, q, st);
+        default: return HT_EUNSUPPORTED;
+    }
+}
+
 template <typename S>
 int chain_prepare(int WP) {  // smem attribute outside any stream capture
     ChainParams<S> dummy{};
     (void)dummy;
+#define HT_PREP(W)                                                                                           \
+    case W:                                                                                                  \
+        CK(cudaFuncSetAttribute(chain_kernel<S, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));  \
+        CK(cudaFuncSetAttribute(chain_kernel2<S, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024)); \
+        break;
     switch (WP) {
-        case 32: CK(cudaFuncSetAttribute(chain_kernel<S, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024)); break;
-        case 64: CK(cudaFuncSetAttribute(chain_kernel<S, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024)); break;
-        case 96: CK(cudaFuncSetAttribute(chain_kernel<S, 96>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024)); break;
-        case 128: CK(cudaFuncSetAttribute(chain_kernel<S, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024)); break;
-        case 160: CK(cudaFuncSetAttribute(chain_kernel<S, 160>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024)); break;
+        HT_PREP(32)
+        HT_PREP(64)
+        HT_PREP(96)
+        HT_PREP(128)
+        HT_PREP(160)
         default: return HT_EUNSUPPORTED;
     }
+#undef HT_PREP
     return HT_OK;
 }
 
@@ -169,13 +201,14 @@ struct Plan {
     int P = 1;        // window merge factor of the apply chains (K2m)
     int nsm = 148;    // SMs (longest-chain-first tile order of the H/T chains)
     bool qz_late = true;   // Q/Z chains of a group start after its H/T chains (HT_QZ_LATE=0: after K2)
+    bool qz_groups = false;  // Q/Z chains as two tile groups per CTA (chain_kernel2; HT_QZ_GROUPS=0: off)
     int hlag = 1;          // helper row split (ChaseArgs::hlag): 0 for r >= 32 (HT_HELPER_LAG overrides)
     size_t mrg_bytes = 0;
     const unsigned long long* gate = nullptr;  // device verdict words of the input check (nullptr: none)
     bool is_root() const { return comm == nullptr || rank == root; }
     bool qz() const { return Q || Z; }
     bool same(const Plan& o) const {
-        return n == o.n && r == o.r && q == o.q && strip_cap == o.strip_cap && helpers == o.helpers && P == o.P && qz_late == o.qz_late && hlag == o.hlag && gate == o.gate && H == o.H && ldh == o.ldh &&
+        return n == o.n && r == o.r && q == o.q && strip_cap == o.strip_cap && helpers == o.helpers && P == o.P && qz_late == o.qz_late && qz_groups == o.qz_groups && hlag == o.hlag && gate == o.gate && H == o.H && ldh == o.ldh &&
                T == o.T && ldt == o.ldt && Q == o.Q && ldq == o.ldq && Z == o.Z && ldz == o.ldz;
     }
 };
@@ -436,7 +469,11 @@ int enqueue_groups(const Plan<S>& p, Workspace<S>& ws, cudaStream_t stream, bool
                                   (p.Q && p.Z) ? 2 : 1, ws.Zr, p.P};
                 pq.gate = p.gate;
                 // persistent grid leaving q whole SMs: the chase of the next group starts at once
-                if (int rc = chain<S>(pq, WP, std::min(pq.njobs * nt, p.qz_ctas), r, q, ws.side, 116 * 1024)) return rc;
+                if (p.qz_groups) {
+                    if (int rc = chain2<S>(pq, WP, std::min((pq.njobs * nt + 1) / 2, p.qz_ctas), r, q, ws.side)) return rc;
+                } else if (int rc = chain<S>(pq, WP, std::min(pq.njobs * nt, p.qz_ctas), r, q, ws.side, 116 * 1024)) {
+                    return rc;
+                }
                 ++g_last_launches;
             }
             if (prof) CK(cudaEventRecord(ev[5 * g + 4], ws.side));
@@ -728,6 +765,9 @@ int run(int64_t n64, int64_t r64, S* H, int64_t ldh, S* T, int64_t ldt, S* Q, in
     pl.hlag = getenv("HT_HELPER_LAG") ? (atoi(getenv("HT_HELPER_LAG")) == 0 ? 0 : 1) : (r >= 32 ? 0 : 1);
     // (measured: configs 2 / 3 / 4 -0.8 / -0.3 / -1.1 % per step; HT_QZ_LATE=0 restores the early start)
     pl.qz_late = !(getenv("HT_QZ_LATE") && atoi(getenv("HT_QZ_LATE")) == 0);
+    // two tile groups per Q/Z CTA where both groups' shared memory fits (one CTA per SM either way)
+    pl.qz_groups = 2 * ((ch_bytes + 127) / 128 * 128) <= (size_t)smem_optin &&
+                   !(getenv("HT_QZ_GROUPS") && atoi(getenv("HT_QZ_GROUPS")) == 0);
     pl.mrg_bytes = mrg_bytes;
     pl.gate = validate ? vs.dflags : nullptr;
     if (comm) {

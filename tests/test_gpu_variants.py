@@ -20,6 +20,7 @@ VARIANTS = [
     {"HT_MERGE": "0"},
     {"HT_NO_GRAPH": "1"},
     {"HT_QZ_LATE": "0"},
+    {"HT_QZ_GROUPS": "0"},  # Q/Z chains one tile per CTA (default: two tile groups per CTA where they fit)
     {"HT_HELPER_LAG": "0"},  # helpers also take the rows just above b0(k) (default only for r >= 32)
     {"HT_HELPER_LAG": "1"},
     {"HT_K1PROF": "1", "HT_K1PROF_T": "1"},  # the instrumented path (profile counters, direct launches)
@@ -39,7 +40,8 @@ def env(request):
 
 
 @pytest.mark.parametrize("env", VARIANTS, indirect=True, ids=lambda d: ",".join(f"{k}={v}" for k, v in d.items()))
-@pytest.mark.parametrize("n,r,q,cplx", [(300, 16, 32, False), (257, 64, 9, False), (200, 8, 12, True)])
+@pytest.mark.parametrize("n,r,q,cplx", [(300, 16, 32, False), (257, 64, 9, False), (200, 8, 12, True),
+                                         (330, 32, 16, False), (300, 128, 9, False)])
 def test_variant_parity(env, n, r, q, cplx):
     H, T = make_pencil(n, r, cplx, seed=97)
     check_parity(H, T, r, q=q)
