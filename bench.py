@@ -304,8 +304,11 @@ def run_reference(args, rank):
 
 
 def _config_dict(args, c, q):
-    d = {"workload": f"config{args.config}: n={c['n']} r={c['r']} {'complex' if c['complex'] else 'real'} fp64, "
-                     f"T diag {'graded 10^U(-3,0)' if c['tdiag'] == 'graded' else '1+|N(0,1)|'}, Q,Z accumulated",
+    td = getattr(args, "tdiag", "") or c["tdiag"]
+    tdt = {"graded": "graded 10^U(-3,0)", "abs": "1+|N(0,1)|",
+           "singular25": "1+|N(0,1)| with 25% exact zeros (singular T, saddle-point-like)"}[td]
+    d = {"workload": f"config{args.config}{'-' + td if td != c['tdiag'] else ''}: n={c['n']} r={c['r']} "
+                     f"{'complex' if c['complex'] else 'real'} fp64, T diag {tdt}, Q,Z accumulated",
          "n": c["n"], "r": c["r"], "complex": c["complex"], "seed": c["seed"],
          "l2": "inputs (4 n^2 fp64) larger than the 126 MB L2; restored from a device copy each step",
          "parallelism": (f"root chase + H/T, Q/Z row slabs x{args.gpus} (NCCL)" if args.gpus > 1 else "1 GPU")}
@@ -326,6 +329,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-check", action="store_true")
+    ap.add_argument("--tdiag", default="", choices=["", "abs", "graded", "singular25"],
+                    help="override the config's T diagonal (singular25: SURVEY 8(f) row 2, saddle-point-like)")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -352,7 +357,8 @@ def main():
     q = args.q or ht.default_q(n, r, cplx)
     tdt = torch.complex128 if cplx else torch.float64
 
-    H_np, T_np = make_pencil(n, r, cplx, c["tdiag"], c["seed"])
+    tdiag = args.tdiag or c["tdiag"]
+    H_np, T_np = make_pencil(n, r, cplx, tdiag, c["seed"])
 
     def col_major_dev(A):
         return torch.from_numpy(A).to(dev)  # Fortran-ordered numpy -> stride (1, n)

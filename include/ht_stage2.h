@@ -147,6 +147,13 @@ int64_t ht_default_q(int64_t n, int64_t r, int is_complex);
  * [3] whole call; and launches[0] = number of kernels launched by it. */
 int ht_last_timing(double *ms_out4, int64_t *launches_out);
 
+/* Debug (environment HT_LAG_CHECK=1, direct launches): the chase kernels stamp every sweep step and
+ * far-strip helper item with the global timer, and the host checks each ordering the wavefront
+ * protocol promises (lag 3 between sweeps; helper items behind their sweep and the
+ * previous sweep's helper).  Returns the number of orderings checked by the LAST call on this host
+ * thread and how many were violated (a step started before the step it waits for had ended). */
+int ht_last_lag_check(int64_t *checked, int64_t *violations);
+
 /* FP64 tensor-core (DMMA) peak probe: runs an mma.sync f64 loop on all SMs for
  * `iters` iterations and returns the achieved TFLOP/s (device-timed). */
 double ht_probe_dmma_tflops(int iters);

@@ -74,6 +74,8 @@ def _load():
     lib.ht_comm_destroy.restype = ctypes.c_int
     lib.ht_slab_range.argtypes = [i64, ctypes.c_int, ctypes.c_int, ctypes.POINTER(i64), ctypes.POINTER(i64)]
     lib.ht_slab_range.restype = ctypes.c_int
+    lib.ht_last_lag_check.argtypes = [ctypes.POINTER(i64), ctypes.POINTER(i64)]
+    lib.ht_last_lag_check.restype = ctypes.c_int
     lib.ht_release_cache.argtypes = []
     lib.ht_release_cache.restype = ctypes.c_int
     _lib = lib
@@ -83,7 +85,7 @@ def _load():
 EXPORTED_SYMBOLS = ("ht_stage2_d", "ht_stage2_z", "ht_stage2_d_ex", "ht_stage2_z_ex",
                     "ht_nccl_unique_id", "ht_comm_create", "ht_comm_destroy", "ht_slab_range", "ht_strerror",
                     "ht_flops_std", "ht_default_q", "ht_last_timing", "ht_probe_dmma_tflops",
-                    "ht_probe_dfma_tflops", "ht_release_cache")
+                    "ht_probe_dfma_tflops", "ht_release_cache", "ht_last_lag_check")
 
 
 def slab_range(n: int, nranks: int, rank: int):
@@ -155,6 +157,13 @@ def last_timing():
     nl = ctypes.c_int64()
     _load().ht_last_timing(ms, ctypes.byref(nl))
     return dict(chase=ms[0], ht_updates=ms[1], qz_updates=ms[2], total=ms[3]), nl.value
+
+
+def last_lag_check():
+    """(orderings checked, violations) of the last call with HT_LAG_CHECK=1 (C ABI ht_last_lag_check)."""
+    a, b = ctypes.c_int64(), ctypes.c_int64()
+    _load().ht_last_lag_check(ctypes.byref(a), ctypes.byref(b))
+    return a.value, b.value
 
 
 def probe_dmma_tflops(iters: int = 20000) -> float:

@@ -47,7 +47,17 @@ struct ChaseArgs {
     int prof_t0;      // >= 0: only sweep prof_t0 of each group records
     int hlag;         // helpers take the band rows above b0(k - hlag): 1, or 0 (see far_strip_helper)
     const unsigned long long* gate;  // input-check verdict (input_rejected)
+    // lag checker (HT_LAG_CHECK, debug): global-timer stamps of every sweep step and helper item,
+    // [start, end] pairs -- sweeps at trace[(t K + k) 2 + 0/1], helpers after qp K pairs at
+    // trace[(qp K + (t H + h) K + k) 2 + 0/1]; checked on the host (ht_stage2.cu, check_lag)
+    unsigned long long* trace;
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 
 __device__ __forceinline__ int ld_acquire(const int* p) {
     int v;
@@ -597,6 +607,7 @@ __device__ __forceinline__ void far_strip_helper(const ChaseArgs<S>& a, int t, i
             }
             (void)ld_acquire(&a.prog[t]);
             if (t > 0) (void)ld_acquire(&hprog[(t - 1) * H + h]);
+            if (a.trace) a.trace[((int64_t)qp * K + ((int64_t)t * H + h) * K + k) * 2] = gtimer();
         }
         __syncthreads();
         if (a.prof && tid == 0) {
@@ -663,6 +674,7 @@ __device__ __forceinline__ void far_strip_helper(const ChaseArgs<S>& a, int t, i
         __syncthreads();
         if (tid == 0) {
             __threadfence();
+            if (a.trace) a.trace[((int64_t)qp * K + ((int64_t)t * H + h) * K + k) * 2 + 1] = gtimer();
             st_release(&hprog[t * H + h], k + 1);
         }
         if (a.prof && tid == 0) {
@@ -806,6 +818,7 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
             }
             __syncthreads();
         }
+        if (a.trace && tid == 0) a.trace[((int64_t)t * K + k) * 2] = gtimer();
         K1_TICK(0);
         S* const ys = (PF && (k & 1)) ? ys1 : ys0;
         S* const Cb = (PF && (k & 1)) ? Cb1 : Cb0;
@@ -1302,6 +1315,7 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
         }
         if (tid == NT - 32) {  // (not thread 0: it spins on the previous sweep meanwhile)
             __threadfence();
+            if (a.trace) a.trace[((int64_t)t * K + k) * 2 + 1] = gtimer();
             st_release(&a.prog[t], k + 1);
         }
         cur ^= 1;

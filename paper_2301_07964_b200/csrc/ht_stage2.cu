@@ -25,6 +25,42 @@ enum { HT_OK = 0, HT_ESTRUCT = 1, HT_ENONFINITE = 2, HT_ECUDA = 3, HT_ENCCL = 4,
 
 thread_local double g_last_ms[4] = {0, 0, 0, 0};
 thread_local int64_t g_last_launches = 0;
+thread_local int64_t g_lag_checked = 0, g_lag_violations = 0;  // HT_LAG_CHECK (ht_last_lag_check)
+
+// Lag checker (debug, HT_LAG_CHECK=1, direct launches): from the global-timer stamps of one
+// chase launch, every ordering the wavefront protocol promises (lag 3 between
+// sweeps, the helpers' items behind their sweep and behind the previous sweep's helper) is checked:
+// a step / item must not start before the step / item it waits for has ended.
+void check_lag(const unsigned long long* tr, int n, int r, int qp, int j1, int K, int H) {
+    auto send = [&](int t, int k) { return tr[((int64_t)t * K + k) * 2 + 1]; };
+    auto sbeg = [&](int t, int k) { return tr[((int64_t)t * K + k) * 2]; };
+    auto hbeg = [&](int t, int h, int k) { return tr[((int64_t)qp * K + ((int64_t)t * H + h) * K + k) * 2]; };
+    auto hend = [&](int t, int h, int k) { return tr[((int64_t)qp * K + ((int64_t)t * H + h) * K + k) * 2 + 1]; };
+    for (int t = 0; t < qp; ++t) {
+        const int j = j1 + t;
+        const int kcount = std::min(K, 2 + (n - j - 1) / r);
+        const int kprev = (t > 0) ? std::min(K, 2 + (n - j) / r) : 0;
+        for (int k = 0; k < kcount; ++k) {
+            if (t > 0) {
+                const int need = std::min(k + 3, kprev), hneed = std::min(k + 2, kprev);
+                ++g_lag_checked;
+                if (sbeg(t, k) < send(t - 1, need - 1)) ++g_lag_violations;
+                for (int h = 0; h < H; ++h) {
+                    ++g_lag_checked;
+                    if (sbeg(t, k) < hend(t - 1, h, hneed - 1)) ++g_lag_violations;
+                }
+            }
+            for (int h = 0; h < H; ++h) {
+                ++g_lag_checked;
+                if (hbeg(t, h, k) < send(t, k)) ++g_lag_violations;
+                if (t > 0) {
+                    ++g_lag_checked;
+                    if (hbeg(t, h, k) < hend(t - 1, h, std::min(k + 2, kprev) - 1)) ++g_lag_violations;
+                }
+            }
+        }
+    }
+}
 
 constexpr int CHASE_NT = 256;
 
@@ -224,6 +260,7 @@ inline int64_t mcatch_st(int q, int r) { return (int64_t)(q + r - 1) * mcatch_ld
 template <typename S>
 struct Workspace {
     S *U[NUV] = {}, *V[NUV] = {}, *MU[NUV] = {}, *MV[NUV] = {}, *Zr = nullptr, *Qr = nullptr, *Tr = nullptr, *Mg = nullptr;
+    unsigned long long* lag = nullptr;  // HT_LAG_CHECK stamps (one group)
     int* prog = nullptr;
     long long* k1prof = nullptr;
     long long k1prof_host[32] = {0};  // [0,16) K1, [16,24) right chains, [24,32) left chains
@@ -253,6 +290,8 @@ struct Workspace {
         CK(mal((void**)&Tr, tf));
         if (chase_dense_catchup<S>(p.r)) CK(mal((void**)&Mg, (size_t)p.Kmax * mcatch_st(p.q, p.r) * sizeof(S)));
         CK(mal((void**)&prog, (size_t)(5 * p.q + 2) * sizeof(int)));
+        if (getenv("HT_LAG_CHECK") && async)
+            CK(mal((void**)&lag, (size_t)2 * p.q * p.Kmax * 4 * sizeof(unsigned long long)));
         if (k1p) {
             CK(mal((void**)&k1prof, 32 * sizeof(long long)));
             CK(cudaMemsetAsync(k1prof, 0, 32 * sizeof(long long), stream));
@@ -290,6 +329,7 @@ struct Workspace {
         Mg = nullptr;
         CK(fr(prog));
         CK(fr(k1prof));
+        CK(fr(lag));
         for (int b = 0; b < NUV; ++b) {
             if (ev_uv[b]) cudaEventDestroy(ev_uv[b]);
             if (ev_qz[b]) cudaEventDestroy(ev_qz[b]);
@@ -404,9 +444,17 @@ int enqueue_groups(const Plan<S>& p, Workspace<S>& ws, cudaStream_t stream, bool
             ChaseArgs<S> ca{n, r, qp, j1, K, p.H, p.ldh, p.T, p.ldt, ws.Qr, ws.Zr, ws.Tr, TLD, ws.Mg,
                             mcatch_ld(q, r), mcatch_st(q, r), ws.prog, p.strip_cap,
                             p.helpers, ws.k1prof, getenv("HT_K1PROF_T") ? atoi(getenv("HT_K1PROF_T")) : -1,
-                            p.hlag, p.gate};
+                            p.hlag, p.gate, ws.lag};
+            const size_t lag_elems = (size_t)2 * qp * K * (1 + p.helpers);
+            if (ws.lag) CK(cudaMemsetAsync(ws.lag, 0, lag_elems * sizeof(unsigned long long), stream));
             void* kargs[] = {&ca};
             CK(cudaLaunchKernel(p.chase_fn, dim3(qp * (1 + p.helpers)), dim3(CHASE_NT), kargs, p.chase_bytes, stream));
+            if (ws.lag) {  // (debug: synchronous per group)
+                std::vector<unsigned long long> h(lag_elems);
+                CK(cudaMemcpyAsync(h.data(), ws.lag, lag_elems * sizeof(unsigned long long), cudaMemcpyDeviceToHost, stream));
+                CK(cudaStreamSynchronize(stream));
+                check_lag(h.data(), n, r, qp, j1, K, p.helpers);
+            }
         }
         if (p.comm && qz) {  // the group's reflectors (2 qp K (r+1) scalars) from the root to every rank
             const size_t cnt = nccl_count<S>((size_t)qp * K * (r + 1));
@@ -638,6 +686,7 @@ template <typename S>
 int run(int64_t n64, int64_t r64, S* H, int64_t ldh, S* T, int64_t ldt, S* Q, int64_t ldq, S* Z,
         int64_t ldz, cudaStream_t stream, ncclComm_t comm, const ht_opts* opts, bool is_complex) {
     g_last_launches = 0;
+    g_lag_checked = g_lag_violations = 0;
     for (double& x : g_last_ms) x = 0;
     // ---- synchronous argument checks (-i = argument i) ----
     if (n64 < 0) return -1;
@@ -781,7 +830,7 @@ int run(int64_t n64, int64_t r64, S* H, int64_t ldh, S* T, int64_t ldt, S* Q, in
     }
     const bool k1p = getenv("HT_K1PROF") != nullptr;
     int rc = HT_OK;
-    if (prof || k1p || comm || getenv("HT_NO_GRAPH")) {
+    if (prof || k1p || comm || getenv("HT_NO_GRAPH") || getenv("HT_LAG_CHECK")) {
         // direct launches (per-kernel-class events / K1 phase counters need them)
         Workspace<S> ws;
         if ((rc = ws.alloc(pl, stream, /*async=*/true, k1p))) return fail(rc);
@@ -904,6 +953,12 @@ double ht_flops_std(int64_t n, int is_complex) {
 }
 
 int64_t ht_default_q(int64_t n, int64_t r, int is_complex) { return default_q(n, r, is_complex); }
+
+int ht_last_lag_check(int64_t* checked, int64_t* violations) {
+    if (checked) *checked = g_lag_checked;
+    if (violations) *violations = g_lag_violations;
+    return HT_OK;
+}
 
 int ht_last_timing(double* ms_out4, int64_t* launches_out) {
     if (ms_out4)

@@ -11,7 +11,9 @@ r-HT pencil):
   (``H(i,j) = 0`` for ``i > j + r``); complex: Re, Im i.i.d. N(0, 1/2).
 * T: upper triangular, N(0,1) strictly-upper entries (complex: N(0,1/2) parts);
   diagonal ``1+|N(0,1)|`` ("abs"), complex ``(1+|N(0,1)|)·e^{iθ}``, θ~U(0,2π),
-  or graded ``10^{U(-3,0)}`` ("graded", config 5).
+  or graded ``10^{U(-3,0)}`` ("graded", config 5), or "singular25": ``1+|N(0,1)|`` with a seeded
+  quarter of the entries exactly 0 (the paper's saddle-point pencils have 25% infinite
+  eigenvalues).
 * Q = Z = I.
 
 Generator: numpy's counter-based Philox bit generator, one stream per
@@ -33,7 +35,7 @@ CONFIGS = {
     5: dict(n=32768, r=128, complex=False, tdiag="graded", seed=1005),
 }
 
-_MID_H, _MID_T, _MID_TD, _MID_TH = 1, 2, 3, 4
+_MID_H, _MID_T, _MID_TD, _MID_TH, _MID_TZ = 1, 2, 3, 4, 5
 
 
 def _rng(seed: int, mid: int, panel: int) -> np.random.Generator:
@@ -68,6 +70,11 @@ def make_pencil(n: int, r: int, complex: bool = False, tdiag: str = "abs", seed:
         d = 10.0 ** rd.uniform(-3.0, 0.0, n)
     else:
         d = 1.0 + np.abs(rd.standard_normal(n))
+    if tdiag == "singular25":
+        # saddle-point-like pencil (25% infinite eigenvalues): a seeded quarter of
+        # T's diagonal is exactly zero, so T is singular and the pencil has n/4 infinite eigenvalues
+        zero = _rng(seed, _MID_TZ, 0).permutation(n)[: n // 4]
+        d[zero] = 0.0
     if complex:
         theta = _rng(seed, _MID_TH, 0).uniform(0.0, 2.0 * np.pi, n)
         d = d * np.exp(1j * theta)
