@@ -45,9 +45,11 @@
  *
  * Multi-GPU (comm != NULL): SPMD -- every rank calls the same function with its
  * own full-size buffers holding identical inputs.  The root (opts->root, default 0) runs the
- * chase and the H/T updates; per group of q sweeps it broadcasts the reflector records over
- * NCCL, every rank forms the window blocks U_k, V_k and updates its row slab of Q and Z
- * (ht_slab_range); at the end the slabs are gathered to the root.  On return H, T, Q, Z are
+ * chase, the left H/T updates and the right H/T updates of the rows near the band; per group of q
+ * sweeps it broadcasts the reflector records over NCCL, every rank forms the window blocks U_k,
+ * V_k, updates its row slab of Q and Z (ht_slab_range) and the right updates of the "far" H/T row
+ * tiles it owns (ht_far_tile_plan: tiles above every later chase band, handed over by the root
+ * point-to-point when they turn far); at the end slabs and far tiles are gathered to the root.  On return H, T, Q, Z are
  * valid on the root only; other ranks' buffers are clobbered.  Argument 13 (opts->root) out of
  * range returns -13.
  *
@@ -97,8 +99,10 @@ typedef struct ht_opts {
 
 #define HT_FLAG_NO_VALIDATE 1
 #define HT_FLAG_PROFILE 2 /* record per-kernel-class device times (ht_last_timing) */
-#define HT_FLAG_EMULATE_SLABS 4 /* comm == NULL: run the Q/Z updates as reserved[0] row slabs (testing the
-                                   multi-GPU decomposition on one GPU) */
+#define HT_FLAG_EMULATE_SLABS 4 /* comm == NULL: run the multi-GPU decomposition as reserved[0] emulated
+                                   ranks on one GPU -- Q/Z as row slabs, far H/T tiles on per-rank
+                                   copies with the hand-offs and the final gather as device copies
+                                   (testing it on one GPU; results bitwise equal to comm == NULL) */
 
 /* Real FP64 stage two.  Arguments 1..12 in order: n, r, H, ldh, T, ldt,
  * Q, ldq, Z, ldz, stream, comm. */
@@ -131,6 +135,13 @@ int ht_release_cache(void);
 /* Multi-GPU row slab: rows [*row0, *row0 + *nrows) (0-based) of Q and Z are updated
  * by `rank` of `nranks` (whole 32-row tiles, balanced).  Host-only; returns 0 or -i. */
 int ht_slab_range(int64_t n, int nranks, int rank, int64_t *row0, int64_t *nrows);
+
+/* Multi-GPU far H/T tiles: row tile `tile` (rows 32 tile .. 32 tile + 31,
+ * 0-based) becomes "far" -- above every later chase band, changed only by the groups' right updates
+ * -- at group *group (j1 = 1 + group q); from then on rank *owner updates it, after the root hands it
+ * the tile's rows at columns >= *col0 (0-based), and the root gathers those back at the end.  Tiles
+ * that never become far: *owner = *group = *col0 = -1.  Host-only; returns 0 or -i. */
+int ht_far_tile_plan(int64_t n, int64_t q, int nranks, int64_t tile, int *owner, int64_t *group, int64_t *col0);
 
 /* Human-readable text for a return code (static storage). */
 const char *ht_strerror(int code);

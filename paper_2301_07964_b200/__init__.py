@@ -76,6 +76,9 @@ def _load():
     lib.ht_slab_range.restype = ctypes.c_int
     lib.ht_last_lag_check.argtypes = [ctypes.POINTER(i64), ctypes.POINTER(i64)]
     lib.ht_last_lag_check.restype = ctypes.c_int
+    lib.ht_far_tile_plan.argtypes = [i64, i64, ctypes.c_int, i64, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(i64),
+                                     ctypes.POINTER(i64)]
+    lib.ht_far_tile_plan.restype = ctypes.c_int
     lib.ht_release_cache.argtypes = []
     lib.ht_release_cache.restype = ctypes.c_int
     _lib = lib
@@ -85,7 +88,7 @@ def _load():
 EXPORTED_SYMBOLS = ("ht_stage2_d", "ht_stage2_z", "ht_stage2_d_ex", "ht_stage2_z_ex",
                     "ht_nccl_unique_id", "ht_comm_create", "ht_comm_destroy", "ht_slab_range", "ht_strerror",
                     "ht_flops_std", "ht_default_q", "ht_last_timing", "ht_probe_dmma_tflops",
-                    "ht_probe_dfma_tflops", "ht_release_cache", "ht_last_lag_check")
+                    "ht_probe_dfma_tflops", "ht_release_cache", "ht_last_lag_check", "ht_far_tile_plan")
 
 
 def slab_range(n: int, nranks: int, rank: int):
@@ -95,6 +98,16 @@ def slab_range(n: int, nranks: int, rank: int):
     if rc != 0:
         raise HTError(rc)
     return a.value, b.value
+
+
+def far_tile_plan(n: int, q: int, nranks: int, tile: int):
+    """(owner, group, col0) of H/T row tile `tile` in the multi-GPU plan (C ABI ht_far_tile_plan);
+    (-1, -1, -1) for tiles that never turn far."""
+    o, g, c = ctypes.c_int(), ctypes.c_int64(), ctypes.c_int64()
+    rc = _load().ht_far_tile_plan(int(n), int(q), int(nranks), int(tile), ctypes.byref(o), ctypes.byref(g), ctypes.byref(c))
+    if rc != 0:
+        raise HTError(rc)
+    return o.value, g.value, c.value
 
 
 def nccl_comm(rank: int, nranks: int, unique_id: bytes):

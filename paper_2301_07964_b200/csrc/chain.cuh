@@ -38,6 +38,7 @@ struct ChainJob {
     int trans;
     int ntiles;
     int tile0;  // first tile of this job (row slab of a multi-GPU rank; 0 = whole matrix)
+    int tstride;  // tiles tile0, tile0 + tstride, ... (far H/T tiles of a rank: the rank count; 0 = 1)
 };
 
 template <typename S>
@@ -205,8 +206,9 @@ __device__ __forceinline__ bool chain_tile(const ChainParams<S>& P, int bid, uns
         const int m0 = P.job[0].mode;
         int band0 = 0, band1 = 0;
         if (m0 == CM_AB_RIGHT && P.stair_first) {  // tiles holding rows j1+1 .. j1+(qp-1) r
-            band0 = min(P.job[0].ntiles, P.j1 / CH_BM);
-            band1 = min(P.job[0].ntiles, (P.j1 + (P.qp - 1) * P.r) / CH_BM + 1);
+            // (tile indices relative to the jobs' first tile; both jobs start at the same tile)
+            band0 = max(0, min(P.job[0].ntiles, P.j1 / CH_BM - P.job[0].tile0));
+            band1 = max(0, min(P.job[0].ntiles, (P.j1 + (P.qp - 1) * P.r) / CH_BM + 1 - P.job[0].tile0));
         }
         chain_order(bid, 2 * P.job[0].ntiles, P.spread, m0 == CM_AB_RIGHT, P.job[0].ntiles, jb_, bid, band0, band1);
     } else if (P.njobs > 1 && bid >= P.job[0].ntiles) {
@@ -216,7 +218,7 @@ __device__ __forceinline__ bool chain_tile(const ChainParams<S>& P, int bid, uns
     const ChainJob<S> J = (jb_ == 0) ? P.job[0] : P.job[1];  // (no dynamic param indexing: no local memory)
     const int mode = J.mode;
     const bool trans = J.trans != 0;
-    const int R0 = (J.tile0 + bid) * CH_BM + 1;  // first tile row (1-based)
+    const int R0 = (J.tile0 + bid * (J.tstride > 0 ? J.tstride : 1)) * CH_BM + 1;  // first tile row (1-based)
     if (R0 > n) return false;
     const int nr = min(CH_BM, n - R0 + 1);
     const int R1 = R0 + nr - 1;

@@ -200,6 +200,17 @@ inline void slab_tiles(int n, int G, int i, int* t0, int* nt) {
     *nt = b - a;
 }
 
+// Far H/T row tiles: tile i (rows CH_BM i .. CH_BM i + CH_BM - 1, 0-based) lies
+// above group g's band once CH_BM (i + 1) <= j1(g) = 1 + g q: no chase of group g or later reads or
+// writes its rows again, and only the groups' right updates (A(1:i5, C_k) V_k, PAPER.md:1895-1900;
+// always the block part, never the staircase) still change it, in columns > j1(g).  From that group
+// on, far tiles are updated by their owner (tile i -> rank i mod G); the root hands the tile's rows
+// (columns >= j1(g), 0-based) to the owner at the start of that group and gathers them back at the
+// end.  Near tiles, the left updates and the chase stay on the root.
+inline int nfar_tiles(int j1, int tiles) { return std::min(tiles, std::max(0, j1) / CH_BM); }
+inline int far_group(int i, int q) { return (CH_BM * (i + 1) - 1 + q - 1) / q; }  // first g with nfar(1+gq) > i
+inline int far_owner(int i, int G) { return i % G; }
+
 template <typename S>
 ncclDataType_t nccl_type() { return ncclFloat64; }
 template <typename S>
@@ -233,6 +244,14 @@ struct Plan {
     // of Q and Z.  comm == nullptr: one GPU (emul > 1 splits the Q/Z chains into emulated slabs).
     ncclComm_t comm = nullptr;
     int rank = 0, nranks = 1, root = 0, emul = 1;
+    // far H/T tiles (nfar_tiles): G owners (NCCL ranks, or emulated ranks on one GPU with their own
+    // full-size H/T copies HR[p], TR[p]; the root's are the caller's buffers)
+    int G = 1;
+    bool emul_ht = false;
+    S* HR[8] = {};
+    S* TR[8] = {};
+    int64_t ldr = 0;
+    bool shard_ht() const { return G > 1; }
     int helpers = 1;  // far-strip helper CTAs per sweep in the chase
     int P = 1;        // window merge factor of the apply chains (K2m)
     int nsm = 148;    // SMs (longest-chain-first tile order of the H/T chains)
@@ -244,7 +263,7 @@ struct Plan {
     bool is_root() const { return comm == nullptr || rank == root; }
     bool qz() const { return Q || Z; }
     bool same(const Plan& o) const {
-        return n == o.n && r == o.r && q == o.q && strip_cap == o.strip_cap && helpers == o.helpers && P == o.P && qz_late == o.qz_late && qz_groups == o.qz_groups && hlag == o.hlag && gate == o.gate && H == o.H && ldh == o.ldh &&
+        return n == o.n && r == o.r && q == o.q && strip_cap == o.strip_cap && helpers == o.helpers && P == o.P && qz_late == o.qz_late && qz_groups == o.qz_groups && hlag == o.hlag && G == o.G && emul_ht == o.emul_ht && gate == o.gate && H == o.H && ldh == o.ldh &&
                T == o.T && ldt == o.ldt && Q == o.Q && ldq == o.ldq && Z == o.Z && ldz == o.ldz;
     }
 };
@@ -261,6 +280,8 @@ template <typename S>
 struct Workspace {
     S *U[NUV] = {}, *V[NUV] = {}, *MU[NUV] = {}, *MV[NUV] = {}, *Zr = nullptr, *Qr = nullptr, *Tr = nullptr, *Mg = nullptr;
     unsigned long long* lag = nullptr;  // HT_LAG_CHECK stamps (one group)
+    S* xfer = nullptr;                  // far H/T tile transfers (2 CH_BM n scalars)
+    S* emu[16] = {};                    // emulated ranks' H/T copies
     int* prog = nullptr;
     long long* k1prof = nullptr;
     long long k1prof_host[32] = {0};  // [0,16) K1, [16,24) right chains, [24,32) left chains
@@ -290,6 +311,7 @@ struct Workspace {
         CK(mal((void**)&Tr, tf));
         if (chase_dense_catchup<S>(p.r)) CK(mal((void**)&Mg, (size_t)p.Kmax * mcatch_st(p.q, p.r) * sizeof(S)));
         CK(mal((void**)&prog, (size_t)(5 * p.q + 2) * sizeof(int)));
+        if (p.shard_ht() && !p.emul_ht) CK(mal((void**)&xfer, (size_t)2 * CH_BM * p.n * sizeof(S)));
         if (getenv("HT_LAG_CHECK") && async)
             CK(mal((void**)&lag, (size_t)2 * p.q * p.Kmax * 4 * sizeof(unsigned long long)));
         if (k1p) {
@@ -330,6 +352,11 @@ struct Workspace {
         CK(fr(prog));
         CK(fr(k1prof));
         CK(fr(lag));
+        CK(fr(xfer));
+        for (auto& e : emu) {
+            CK(fr(e));
+            e = nullptr;
+        }
         for (int b = 0; b < NUV; ++b) {
             if (ev_uv[b]) cudaEventDestroy(ev_uv[b]);
             if (ev_qz[b]) cudaEventDestroy(ev_qz[b]);
@@ -414,6 +441,57 @@ int gather_slabs(const Plan<S>& p, cudaStream_t stream) {
     return HT_OK;
 }
 
+// Rows [r0, r0 + len) x columns [c0, n) (0-based) of H and T from rank `src` to rank `dst`:
+// emulated ranks -- a 2-D copy between their buffers; NCCL -- pack, send / recv, unpack (stream-
+// ordered on `stream`; the calling rank takes its part; point-to-point calls outside NCCL groups so
+// that the unpack follows the receive on the stream).  buf: workspace of 2 len (n - c0) scalars.
+template <typename S>
+int move_rows_ht(const Plan<S>& p, int src, int dst, int r0, int len, int c0, S* buf, cudaStream_t stream) {
+    const int n = p.n, nc = n - c0;
+    if (len <= 0 || nc <= 0 || src == dst) return HT_OK;
+    if (p.emul_ht) {
+        for (int m = 0; m < 2; ++m) {
+            S* a = m ? p.TR[src] : p.HR[src];
+            S* b = m ? p.TR[dst] : p.HR[dst];
+            const int64_t lda = src == p.root ? (m ? p.ldt : p.ldh) : p.ldr;
+            const int64_t ldb = dst == p.root ? (m ? p.ldt : p.ldh) : p.ldr;
+            CK(cudaMemcpy2DAsync(b + r0 + (int64_t)c0 * ldb, ldb * sizeof(S), a + r0 + (int64_t)c0 * lda, lda * sizeof(S),
+                                 len * sizeof(S), nc, cudaMemcpyDeviceToDevice, stream));
+        }
+        return HT_OK;
+    }
+    const size_t cnt = (size_t)len * nc;
+    if (p.rank == src) {
+        pack_rows_kernel<S><<<4 * 148, 256, 0, stream>>>(p.H + (int64_t)c0 * p.ldh, p.ldh, r0, len, nc, buf);
+        pack_rows_kernel<S><<<4 * 148, 256, 0, stream>>>(p.T + (int64_t)c0 * p.ldt, p.ldt, r0, len, nc, buf + cnt);
+        CK(cudaGetLastError());
+        NK(ncclSend(buf, nccl_count<S>(2 * cnt), nccl_type<S>(), dst, p.comm, stream));
+    } else if (p.rank == dst) {
+        NK(ncclRecv(buf, nccl_count<S>(2 * cnt), nccl_type<S>(), src, p.comm, stream));
+        unpack_rows_kernel<S><<<4 * 148, 256, 0, stream>>>(p.H + (int64_t)c0 * p.ldh, p.ldh, r0, len, nc, buf);
+        unpack_rows_kernel<S><<<4 * 148, 256, 0, stream>>>(p.T + (int64_t)c0 * p.ldt, p.ldt, r0, len, nc, buf + cnt);
+        CK(cudaGetLastError());
+    }
+    return HT_OK;
+}
+
+// Far H/T tiles back to the root at the end: every far tile owned by a non-root rank, its rows and
+// the columns >= j1 of the group at which it became far.
+template <typename S>
+int gather_far_ht(const Plan<S>& p, S* buf, cudaStream_t stream) {
+    const int n = p.n, q = p.q, tiles = (n + CH_BM - 1) / CH_BM;
+    const int ngroups = (n - 2 + q - 1) / q;
+    for (int i = 0; i < tiles; ++i) {
+        const int g = far_group(i, q);
+        if (g >= ngroups) break;  // (tiles become far in order)
+        const int o = far_owner(i, p.G);
+        if (o == p.root) continue;
+        const int r0 = i * CH_BM, len = std::min(CH_BM, n - r0), c0 = 1 + g * q;  // (0-based column j1(g))
+        if (int rc = move_rows_ht<S>(p, o, p.root, r0, len, c0, buf, stream)) return rc;
+    }
+    return HT_OK;
+}
+
 template <typename S>
 int enqueue_groups(const Plan<S>& p, Workspace<S>& ws, cudaStream_t stream, bool prof) {
     const int n = p.n, r = p.r, q = p.q, WP = p.WP, LDB = p.LDB, TLD = q;
@@ -436,6 +514,14 @@ int enqueue_groups(const Plan<S>& p, Workspace<S>& ws, cudaStream_t stream, bool
         const int K = 1 + (n - j1 - 2) / r;
         const int bsel = qz ? (g % NUV) : 0;
         const bool root = p.is_root();
+        const int tiles = (n + CH_BM - 1) / CH_BM;
+        const int nf = p.shard_ht() ? nfar_tiles(j1, tiles) : 0;  // far H/T tiles of this group
+        if (p.shard_ht())  // tiles turned far by this group: root -> owner (after the root's updates of g-1)
+            for (int i = nfar_tiles(j1 - q, tiles); i < nf; ++i) {
+                const int r0 = i * CH_BM;
+                if (int rc = move_rows_ht<S>(p, p.root, far_owner(i, p.G), r0, std::min(CH_BM, n - r0), j1, ws.xfer, stream))
+                    return rc;
+            }
         if (prof) CK(cudaEventRecord(ev[5 * g + 0], stream));
         if (root) {
             CK(cudaMemsetAsync(ws.prog, 0, (size_t)((1 + p.helpers) * q + 1) * sizeof(int), stream));
@@ -456,7 +542,7 @@ int enqueue_groups(const Plan<S>& p, Workspace<S>& ws, cudaStream_t stream, bool
                 check_lag(h.data(), n, r, qp, j1, K, p.helpers);
             }
         }
-        if (p.comm && qz) {  // the group's reflectors (2 qp K (r+1) scalars) from the root to every rank
+        if (p.comm && (qz || p.shard_ht())) {  // the group's reflectors (2 qp K (r+1) scalars) to every rank
             const size_t cnt = nccl_count<S>((size_t)qp * K * (r + 1));
             NK(ncclGroupStart());
             NK(ncclBroadcast(ws.Qr, ws.Qr, cnt, nccl_type<S>(), p.root, p.comm, stream));
@@ -466,7 +552,7 @@ int enqueue_groups(const Plan<S>& p, Workspace<S>& ws, cudaStream_t stream, bool
         if (qz && g >= NUV) CK(cudaStreamWaitEvent(stream, ws.ev_qz[bsel], 0));  // Q/Z of g-NUV done with U/V[bsel]
         AccumArgs<S> aa{n, r, qp, j1, K, WP, LDB, p.acc_bytes >= accum_smem_bytes<S>(r, q, true) ? 1 : 0, ws.Qr, ws.Zr,
                         ws.U[bsel], ws.V[bsel], p.gate};
-        if (root || qz) {
+        if (root || qz || p.shard_ht()) {
             accum_kernel<S, ACC_NT><<<dim3(K, 2), ACC_NT, p.acc_bytes, stream>>>(aa);
             CK(cudaGetLastError());
             g_last_launches += 2;
@@ -482,15 +568,31 @@ int enqueue_groups(const Plan<S>& p, Workspace<S>& ws, cudaStream_t stream, bool
         if (qz && !p.qz_late) CK(cudaEventRecord(ws.ev_uv[bsel], stream));
         if (prof) CK(cudaEventRecord(ev[5 * g + 1], stream));
         // ---- apply phase: right updates of H, T (staircase + V_k), then left (U_k^*) ----
-        const int tiles = (n + CH_BM - 1) / CH_BM;
+        // far tiles (rows above the band): every owner updates its own (tile i -> rank i mod G)
+        if (nf > 0)
+            for (int rk = 0; rk < p.G; ++rk) {
+                if (!p.emul_ht && rk != p.rank) continue;
+                const int cnt = rk < nf ? (nf - rk + p.G - 1) / p.G : 0;
+                if (cnt == 0) continue;
+                S* Hk = p.emul_ht ? p.HR[rk] : p.H;
+                S* Tk = p.emul_ht ? p.TR[rk] : p.T;
+                const int64_t lhk = (p.emul_ht && rk != p.root) ? p.ldr : p.ldh;
+                const int64_t ltk = (p.emul_ht && rk != p.root) ? p.ldr : p.ldt;
+                ChainParams<S> pf{n, r, qp, j1, K, {{Hk, lhk, ws.V[bsel], ws.MV[bsel], CM_AB_RIGHT, 0, cnt, rk, p.G},
+                                                    {Tk, ltk, ws.V[bsel], ws.MV[bsel], CM_AB_RIGHT, 0, cnt, rk, p.G}}, 2, ws.Zr, p.P,
+                                  0};
+                pf.gate = p.gate;
+                if (int rc = chain<S>(pf, WP, 2 * cnt, r, q, stream)) return rc;
+                ++g_last_launches;
+            }
         if (root) {
-            ChainParams<S> pr{n, r, qp, j1, K, {{p.H, p.ldh, ws.V[bsel], ws.MV[bsel], CM_AB_RIGHT, 0, tiles, 0},
-                                                {p.T, p.ldt, ws.V[bsel], ws.MV[bsel], CM_AB_RIGHT, 0, tiles, 0}}, 2, ws.Zr, p.P,
+            ChainParams<S> pr{n, r, qp, j1, K, {{p.H, p.ldh, ws.V[bsel], ws.MV[bsel], CM_AB_RIGHT, 0, tiles - nf, nf},
+                                                {p.T, p.ldt, ws.V[bsel], ws.MV[bsel], CM_AB_RIGHT, 0, tiles - nf, nf}}, 2, ws.Zr, p.P,
                               chain_spread(p.nsm), ws.k1prof ? ws.k1prof + 16 : nullptr,
                               getenv("HT_CHAIN_PROF_TILE") ? atoi(getenv("HT_CHAIN_PROF_TILE")) : 0,
                               !(getenv("HT_STAIR_FIRST") && atoi(getenv("HT_STAIR_FIRST")) == 0)};
             pr.gate = p.gate;
-            if (int rc = chain<S>(pr, WP, 2 * tiles, r, q, stream)) return rc;
+            if (int rc = chain<S>(pr, WP, 2 * (tiles - nf), r, q, stream)) return rc;
             ChainParams<S> pl{n, r, qp, j1, K, {{p.H, p.ldh, ws.U[bsel], ws.MU[bsel], CM_A_LEFT, 1, tiles, 0},
                                                 {p.T, p.ldt, ws.U[bsel], ws.MU[bsel], CM_B_LEFT, 1, tiles, 0}}, 2, ws.Zr, p.P,
                               chain_spread(p.nsm), ws.k1prof ? ws.k1prof + 24 : nullptr,
@@ -534,6 +636,8 @@ int enqueue_groups(const Plan<S>& p, Workspace<S>& ws, cudaStream_t stream, bool
     }
     if (p.comm && qz && p.nranks > 1)
         if (int rc = gather_slabs<S>(p, stream)) return rc;
+    if (p.shard_ht())
+        if (int rc = gather_far_ht<S>(p, ws.xfer, stream)) return rc;
     if (prof) {
         CK(cudaStreamSynchronize(stream));
         double acc[3] = {0, 0, 0};
@@ -825,15 +929,38 @@ int run(int64_t n64, int64_t r64, S* H, int64_t ldh, S* T, int64_t ldt, S* Q, in
         NK(ncclCommUserRank(comm, &pl.rank));
         pl.root = opts ? opts->root : 0;
         if (pl.root < 0 || pl.root >= pl.nranks) return refuse(-13);
+        // far H/T tiles sharded over the ranks (HT_SHARD_HT=0: Q/Z slabs only)
+        if (!(getenv("HT_SHARD_HT") && atoi(getenv("HT_SHARD_HT")) == 0)) pl.G = pl.nranks;
     } else if (opts && (opts->flags & HT_FLAG_EMULATE_SLABS)) {
         pl.emul = std::max(1, opts->reserved[0]);
+        // the same decomposition as emul ranks on this GPU: Q/Z slabs on the caller's buffers, far
+        // H/T tiles on per-rank copies (NaN-filled: a tile used before its hand-off poisons the result)
+        pl.G = std::min(8, pl.emul);
+        pl.emul_ht = pl.G > 1;
     }
     const bool k1p = getenv("HT_K1PROF") != nullptr;
     int rc = HT_OK;
-    if (prof || k1p || comm || getenv("HT_NO_GRAPH") || getenv("HT_LAG_CHECK")) {
+    if (prof || k1p || comm || pl.emul_ht || getenv("HT_NO_GRAPH") || getenv("HT_LAG_CHECK")) {
         // direct launches (per-kernel-class events / K1 phase counters need them)
         Workspace<S> ws;
         if ((rc = ws.alloc(pl, stream, /*async=*/true, k1p))) return fail(rc);
+        if (pl.emul_ht) {
+            pl.ldr = n;
+            pl.HR[0] = H;
+            pl.TR[0] = T;
+            CK(cudaMallocAsync((void**)&ws.xfer, (size_t)2 * CH_BM * n * sizeof(S), stream));
+            for (int k = 1; k < pl.G; ++k) {
+                for (int m = 0; m < 2; ++m) {
+                    if (cudaMallocAsync((void**)&ws.emu[2 * k + m], (size_t)n * n * sizeof(S), stream) != cudaSuccess) {
+                        ws.release(stream, true);
+                        return fail(HT_ENOMEM);
+                    }
+                    CK(cudaMemsetAsync(ws.emu[2 * k + m], 0xff, (size_t)n * n * sizeof(S), stream));
+                }
+                pl.HR[k] = ws.emu[2 * k];
+                pl.TR[k] = ws.emu[2 * k + 1];
+            }
+        }
         rc = enqueue_groups<S>(pl, ws, stream, prof);
         if (int rf = ws.release(stream, /*async=*/true)) rc = rc ? rc : rf;
         if (rc) return fail(rc);
@@ -926,6 +1053,21 @@ int ht_release_cache(void) {
     if (int r2 = release_graphs<zc>()) rc = rc ? rc : r2;
     if (int r3 = release_val_states()) rc = rc ? rc : r3;
     return rc;
+}
+
+int ht_far_tile_plan(int64_t n, int64_t q, int nranks, int64_t tile, int* owner, int64_t* group, int64_t* col0) {
+    if (n < 0) return -1;
+    if (q < 1) return -2;
+    if (nranks < 1) return -3;
+    if (tile < 0) return -4;
+    if (!owner || !group || !col0) return -5;
+    const int64_t ngroups = n > 2 ? (n - 2 + q - 1) / q : 0;
+    const int64_t g = far_group((int)tile, (int)q);
+    const bool far = tile * CH_BM < n && g < ngroups;
+    *owner = far ? far_owner((int)tile, nranks) : -1;
+    *group = far ? g : -1;
+    *col0 = far ? 1 + g * q : -1;
+    return HT_OK;
 }
 
 int ht_comm_destroy(ncclComm_t comm) {

@@ -132,3 +132,77 @@ def test_slabs_across_gloo_ranks(ht):
     slabs = views[0][0]
     assert slabs[0][0] == 0 and slabs[0][0] + slabs[0][1] == slabs[1][0] and slabs[1][0] + slabs[1][1] == n
     assert views[1][1] == b"x" * 128
+
+
+# ---------------------------------------------------------------------------- far H/T tile plan (§8(e))
+def _far_plan_worker(rank, world, port, n, q, out):
+    import torch
+    import torch.distributed as dist
+    import paper_2301_07964_b200 as ht
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    tiles = (n + 31) // 32
+    plan = [ht.far_tile_plan(n, q, world, t) for t in range(tiles)]
+    root = 0
+    # this rank's message schedule, in issue order: hand-offs group by group, then the final gather
+    sends, recvs = [], []
+    for g in range((n - 2 + q - 1) // q):
+        for t, (o, gt, c0) in enumerate(plan):
+            if gt == g and o != root:
+                msg = ("handoff", g, t, c0)
+                if rank == root:
+                    sends.append((o,) + msg)
+                if rank == o:
+                    recvs.append((root,) + msg)
+    for t, (o, gt, c0) in enumerate(plan):
+        if o not in (-1, root):
+            msg = ("gather", gt, t, c0)
+            if rank == o:
+                sends.append((root,) + msg)
+            if rank == root:
+                recvs.append((o,) + msg)
+    allp = [None] * world
+    dist.all_gather_object(allp, {"plan": plan, "sends": sends, "recvs": recvs})
+    out.put((rank, allp))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n,q,world", [(1000, 32, 2), (777, 13, 3)])
+def test_far_tile_plan_across_gloo_ranks(n, q, world):
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    qu = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_far_plan_worker, args=(r, world, port, n, q, qu)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = dict(qu.get(timeout=180) for _ in range(world))
+    for p in ps:
+        p.join(timeout=60)
+    views = res[0]
+    assert all(res[r] == views for r in range(world))  # every rank saw the same exchange
+    plans = [v["plan"] for v in views]
+    assert all(pl == plans[0] for pl in plans)  # one deterministic plan on every rank
+    plan = plans[0]
+    tiles = (n + 31) // 32
+    ngroups = (n - 2 + q - 1) // q
+    far = [t for t, (o, g, c) in enumerate(plan) if o >= 0]
+    # a tile turns far at the first group whose j1 = 1 + g q is at or below its last row + 1, once
+    for t, (o, g, c) in enumerate(plan):
+        if o < 0:
+            assert 1 + (ngroups - 1) * q < 32 * (t + 1)
+            continue
+        assert o == t % world and c == 1 + g * q and 32 * (t + 1) <= c and (g == 0 or 1 + (g - 1) * q < 32 * (t + 1))
+    assert far == list(range(len(far)))  # far tiles are a prefix, turning far in order
+    owned = [sum(1 for t in far if plan[t][0] == r) for r in range(world)]
+    assert max(owned) - min(owned) <= 1  # balanced
+    # every send has exactly one matching receive, in the same order between each pair of ranks
+    for a in range(world):
+        for b in range(world):
+            s_ab = [m[1:] for m in views[a]["sends"] if m[0] == b]
+            r_ba = [m[1:] for m in views[b]["recvs"] if m[0] == a]
+            assert s_ab == r_ba, (a, b)
+    # each far tile not owned by the root is handed off once and gathered back once
+    hand = sorted(m[3] for m in views[0]["sends"] if m[1] == "handoff")
+    gath = sorted(m[3] for m in views[0]["recvs"] if m[1] == "gather")
+    assert hand == gath == [t for t in far if plan[t][0] != 0]
+    assert tiles > len(far) > 0

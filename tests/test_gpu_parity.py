@@ -248,17 +248,24 @@ def test_release_cache_then_call_again():
 # share a GPU, so the N>1 path is checked by (a) the same Q/Z row-slab decomposition run as
 # emulated slabs on one GPU, and (b) the NCCL path itself with a single-rank communicator.
 
-@pytest.mark.parametrize("slabs", [2, 3, 8])
-def test_emulated_row_slabs_bitwise_equal(slabs):
+@pytest.mark.parametrize("n,r,q,cplx,ranks", [(300, 10, 12, False, 2), (300, 10, 12, False, 3), (300, 10, 12, False, 8),
+                                               (700, 16, 8, False, 4), (640, 64, 32, False, 3), (400, 8, 9, True, 2),
+                                               (500, 128, 16, False, 2)])
+def test_emulated_ranks_bitwise_equal(n, r, q, cplx, ranks):
+    # the multi-GPU decomposition as emulated ranks on one GPU: Q/Z row slabs, and far H/T row tiles
+    # on per-rank NaN-filled copies with the hand-offs and the final gather as device copies -- a
+    # tile updated before its hand-off or missed by the gather would poison or stale the result
     ht = _ht()
-    H, T = make_pencil(300, 10, seed=31)
+    H, T = make_pencil(n, r, cplx, seed=31)
     outs = []
-    for emu in (0, slabs):
+    for emu in (0, ranks):
         Hd, Td = _dev(H), _dev(T)
-        Qd, Zd = _dev(np.eye(300)), _dev(np.eye(300))
-        ht.ht_stage2(Hd, Td, 10, Qd, Zd, q=12, emulate_slabs=emu)
+        Qd, Zd = _dev(np.eye(n, dtype=H.dtype)), _dev(np.eye(n, dtype=H.dtype))
+        ht.ht_stage2(Hd, Td, r, Qd, Zd, q=q, emulate_slabs=emu)
         torch.cuda.synchronize()
         outs.append([_host(X) for X in (Hd, Td, Qd, Zd)])
+    far = [ht.far_tile_plan(n, q, ranks, t) for t in range((n + 31) // 32)]
+    assert sum(1 for o, _, _ in far if o > 0) > 0  # the case really moves tiles
     for a, b in zip(*outs):
         assert np.array_equal(a, b)
 
