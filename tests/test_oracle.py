@@ -287,3 +287,22 @@ def test_worked_example_n4_r2():
     a = normalize_phase(h, t, q, z)
     b = normalize_phase(hg, tg, qg, zg)
     assert max(rel_diff(x, y) for x, y in zip(a, b)) < 1e-14
+
+
+# ----------------------------------------------------------------------------- blocked == unblocked
+@pytest.mark.parametrize("n,r,q,cplx", [(60, 4, 6, False), (97, 6, 5, False), (80, 5, 8, False), (64, 8, 1, False),
+                                         (72, 3, 12, True), (90, 4, 9, True)])
+def test_blocked_schedule_matches_oracle(n, r, q, cplx):
+    # SURVEY §8(c) pin 6: the corrected blocked Alg. 3/4 (App. A.2-A.3; tests/blocked_ref.py, a second
+    # CPU ordering sharing no code with oracle/) reorders Alg. 2's reflector applications only as
+    # PAPER.md:720-732 allows, so it must give the oracle's result up to rounding -- this pins the
+    # index corrections (reading c8) the GPU kernels implement, independently of the GPU
+    from blocked_ref import blocked_stage2
+    H, T = make_pencil(n, r, cplx, seed=500 + n)
+    ho, to, qo, zo, _ = oracle.stage2(H, T, r)
+    hb, tb, qb, zb = blocked_stage2(H, T, r, q)
+    a = normalize_phase(hb, tb, qb, zb)
+    b = normalize_phase(ho, to, qo, zo)
+    assert max(rel_diff(x, y) for x, y in zip(a, b)) < 1e-12
+    inv = invariants(H, T, hb, tb, qb, zb)
+    assert inv["zeros_bad"] == 0 and max(inv["eA"], inv["eB"], inv["oQ"], inv["oZ"]) <= inv["bound"]
