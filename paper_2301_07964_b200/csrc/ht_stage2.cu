@@ -257,13 +257,14 @@ struct Plan {
     int nsm = 148;    // SMs (longest-chain-first tile order of the H/T chains)
     bool qz_late = true;   // Q/Z chains of a group start after its H/T chains (HT_QZ_LATE=0: after K2)
     bool qz_groups = false;  // Q/Z chains as two tile groups per CTA (chain_kernel2; HT_QZ_GROUPS=0: off)
+    bool far_side = false;   // one GPU: far H/T tiles' right updates on the side stream (HT_FAR_SIDE)
     int hlag = 1;          // helper row split (ChaseArgs::hlag): 0 for r >= 32 (HT_HELPER_LAG overrides)
     size_t mrg_bytes = 0;
     const unsigned long long* gate = nullptr;  // device verdict words of the input check (nullptr: none)
     bool is_root() const { return comm == nullptr || rank == root; }
     bool qz() const { return Q || Z; }
     bool same(const Plan& o) const {
-        return n == o.n && r == o.r && q == o.q && strip_cap == o.strip_cap && helpers == o.helpers && P == o.P && qz_late == o.qz_late && qz_groups == o.qz_groups && hlag == o.hlag && G == o.G && emul_ht == o.emul_ht && gate == o.gate && H == o.H && ldh == o.ldh &&
+        return n == o.n && r == o.r && q == o.q && strip_cap == o.strip_cap && helpers == o.helpers && P == o.P && qz_late == o.qz_late && qz_groups == o.qz_groups && far_side == o.far_side && hlag == o.hlag && G == o.G && emul_ht == o.emul_ht && gate == o.gate && H == o.H && ldh == o.ldh &&
                T == o.T && ldt == o.ldt && Q == o.Q && ldq == o.ldq && Z == o.Z && ldz == o.ldz;
     }
 };
@@ -286,7 +287,7 @@ struct Workspace {
     long long* k1prof = nullptr;
     long long k1prof_host[32] = {0};  // [0,16) K1, [16,24) right chains, [24,32) left chains
     cudaStream_t side = nullptr;
-    cudaEvent_t ev_uv[NUV] = {}, ev_qz[NUV] = {};
+    cudaEvent_t ev_uv[NUV] = {}, ev_qz[NUV] = {}, ev_k2[NUV] = {};
     bool async = true;
 
     int alloc(const Plan<S>& p, cudaStream_t stream, bool async_, bool k1p) {
@@ -325,6 +326,7 @@ struct Workspace {
             for (int b = 0; b < NUV; ++b) {
                 CK(cudaEventCreateWithFlags(&ev_uv[b], cudaEventDisableTiming));
                 CK(cudaEventCreateWithFlags(&ev_qz[b], cudaEventDisableTiming));
+                CK(cudaEventCreateWithFlags(&ev_k2[b], cudaEventDisableTiming));
             }
         }
         return HT_OK;
@@ -360,6 +362,7 @@ struct Workspace {
         for (int b = 0; b < NUV; ++b) {
             if (ev_uv[b]) cudaEventDestroy(ev_uv[b]);
             if (ev_qz[b]) cudaEventDestroy(ev_qz[b]);
+            if (ev_k2[b]) cudaEventDestroy(ev_k2[b]);
         }
         if (side) cudaStreamDestroy(side);  // deferred until its work completes
         return HT_OK;
@@ -515,7 +518,8 @@ int enqueue_groups(const Plan<S>& p, Workspace<S>& ws, cudaStream_t stream, bool
         const int bsel = qz ? (g % NUV) : 0;
         const bool root = p.is_root();
         const int tiles = (n + CH_BM - 1) / CH_BM;
-        const int nf = p.shard_ht() ? nfar_tiles(j1, tiles) : 0;  // far H/T tiles of this group
+        // far H/T tiles of this group: owned by the ranks (multi-GPU), or updated on the side stream
+        const int nf = (p.shard_ht() || p.far_side) ? nfar_tiles(j1, tiles) : 0;
         if (p.shard_ht())  // tiles turned far by this group: root -> owner (after the root's updates of g-1)
             for (int i = nfar_tiles(j1 - q, tiles); i < nf; ++i) {
                 const int r0 = i * CH_BM;
@@ -566,10 +570,27 @@ int enqueue_groups(const Plan<S>& p, Workspace<S>& ws, cudaStream_t stream, bool
         // Q/Z chains of group g start after K2 (their blocks), or -- p.qz_late -- after the group's
         // H/T chains, so that those (on the critical path) do not share SMs with them
         if (qz && !p.qz_late) CK(cudaEventRecord(ws.ev_uv[bsel], stream));
+        if (p.far_side && nf > 0) {
+            // one GPU: the far tiles' right updates (rows above every later chase band, SURVEY
+            // §8(a) a7) need only U/V of this group and the tiles' state after group g-1 (main stream,
+            // before this group's chase), so they run on the side stream beside this group's near
+            // H/T chains and the next chase, as a persistent grid on the SMs the chase leaves
+            CK(cudaEventRecord(ws.ev_k2[bsel], stream));
+            CK(cudaStreamWaitEvent(ws.side, ws.ev_k2[bsel], 0));
+            ChainParams<S> pf{n, r, qp, j1, K, {{p.H, p.ldh, ws.V[bsel], ws.MV[bsel], CM_AB_RIGHT, 0, nf, 0},
+                                                {p.T, p.ldt, ws.V[bsel], ws.MV[bsel], CM_AB_RIGHT, 0, nf, 0}}, 2, ws.Zr, p.P, 0};
+            pf.gate = p.gate;
+            if (p.qz_groups) {
+                if (int rc = chain2<S>(pf, WP, std::min(nf, p.qz_ctas), r, q, ws.side)) return rc;
+            } else if (int rc = chain<S>(pf, WP, std::min(2 * nf, p.qz_ctas), r, q, ws.side, 116 * 1024)) {
+                return rc;
+            }
+            ++g_last_launches;
+        }
         if (prof) CK(cudaEventRecord(ev[5 * g + 1], stream));
         // ---- apply phase: right updates of H, T (staircase + V_k), then left (U_k^*) ----
         // far tiles (rows above the band): every owner updates its own (tile i -> rank i mod G)
-        if (nf > 0)
+        if (nf > 0 && p.shard_ht())
             for (int rk = 0; rk < p.G; ++rk) {
                 if (!p.emul_ht && rk != p.rank) continue;
                 const int cnt = rk < nf ? (nf - rk + p.G - 1) / p.G : 0;
@@ -921,6 +942,7 @@ int run(int64_t n64, int64_t r64, S* H, int64_t ldh, S* T, int64_t ldt, S* Q, in
     // two tile groups per Q/Z CTA where both groups' shared memory fits (one CTA per SM either way)
     pl.qz_groups = 2 * ((ch_bytes + 127) / 128 * 128) <= (size_t)smem_optin &&
                    !(getenv("HT_QZ_GROUPS") && atoi(getenv("HT_QZ_GROUPS")) == 0);
+    pl.far_side = (Q || Z) && getenv("HT_FAR_SIDE") && atoi(getenv("HT_FAR_SIDE")) != 0;
     pl.mrg_bytes = mrg_bytes;
     pl.gate = validate ? vs.dflags : nullptr;
     if (comm) {

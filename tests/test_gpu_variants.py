@@ -20,7 +20,8 @@ VARIANTS = [
     {"HT_MERGE": "0"},
     {"HT_NO_GRAPH": "1"},
     {"HT_QZ_LATE": "0"},
-    {"HT_QZ_GROUPS": "0"},  # Q/Z chains one tile per CTA (default: two tile groups per CTA where they fit)
+    {"HT_QZ_GROUPS": "0"},
+    {"HT_FAR_SIDE": "1"},  # one GPU: far H/T tiles' right updates on the side stream  # Q/Z chains one tile per CTA (default: two tile groups per CTA where they fit)
     {"HT_HELPER_LAG": "0"},  # helpers also take the rows just above b0(k) (default only for r >= 32)
     {"HT_HELPER_LAG": "1"},
     {"HT_K1PROF": "1", "HT_K1PROF_T": "1"},  # the instrumented path (profile counters, direct launches)
