@@ -942,7 +942,6 @@ int run(int64_t n64, int64_t r64, S* H, int64_t ldh, S* T, int64_t ldt, S* Q, in
     // two tile groups per Q/Z CTA where both groups' shared memory fits (one CTA per SM either way)
     pl.qz_groups = 2 * ((ch_bytes + 127) / 128 * 128) <= (size_t)smem_optin &&
                    !(getenv("HT_QZ_GROUPS") && atoi(getenv("HT_QZ_GROUPS")) == 0);
-    pl.far_side = (Q || Z) && getenv("HT_FAR_SIDE") && atoi(getenv("HT_FAR_SIDE")) != 0;
     pl.mrg_bytes = mrg_bytes;
     pl.gate = validate ? vs.dflags : nullptr;
     if (comm) {
@@ -960,6 +959,10 @@ int run(int64_t n64, int64_t r64, S* H, int64_t ldh, S* T, int64_t ldt, S* Q, in
         pl.G = std::min(8, pl.emul);
         pl.emul_ht = pl.G > 1;
     }
+    // far H/T tiles on the side stream (one GPU): measured -2 % per step at configs 4 and 5 (r = 64,
+    // 128), +1 % / +2 % at configs 2 and 3 -- on by default for real r >= 64 (HT_FAR_SIDE overrides)
+    pl.far_side = (Q || Z) && !comm && !pl.emul_ht &&
+                  (getenv("HT_FAR_SIDE") ? atoi(getenv("HT_FAR_SIDE")) != 0 : (sizeof(S) == 8 && r >= 64));
     const bool k1p = getenv("HT_K1PROF") != nullptr;
     int rc = HT_OK;
     if (prof || k1p || comm || pl.emul_ht || getenv("HT_NO_GRAPH") || getenv("HT_LAG_CHECK")) {

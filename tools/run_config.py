@@ -26,7 +26,10 @@ def main():
     ap.add_argument("--q", type=int, default=0)
     ap.add_argument("--n", type=int, default=0)
     ap.add_argument("--no-check", action="store_true")
+    ap.add_argument("--lib", default="", help="A/B: another build of libht_stage2.so")
     args = ap.parse_args()
+    if args.lib:
+        ht._SO = args.lib
     c = CONFIGS[args.cfg]
     Hn, Tn = config_pencil(args.cfg, args.n or None)
     n, r = Hn.shape[0], c["r"]
