@@ -187,6 +187,9 @@ __device__ __forceinline__ S lpr_sum(S v) {
     return v;
 }
 
+#ifndef HT_RQ_ATTR
+#define HT_RQ_ATTR __forceinline__
+#endif
 // Householder RQ (readings c3/c4), rows bottom-up (xGERQ2 order) on C = B(i1:i2,i1:i2) (m x m,
 // col-major, ld LDC) with P = I alongside.  Stage i (i = m-1 .. 1, plus 0 for complex) generates
 // H_i from row i of C (alpha = conj(C[i][i]), tail conj(C[i][0..i)): oracle_rq_first_row's larfg)
@@ -197,7 +200,7 @@ __device__ __forceinline__ S lpr_sum(S v) {
 // s = |alpha|^2 + |tail|^2).  Column i is dead after stage i (later stages act on columns < i,
 // the output is column 0), so it is not updated.  ring: m slots of PLD; flag: volatile counter.
 template <typename S, int MAXM>
-__device__ __forceinline__ void rq_direction(int m, const S* Cb, int LDC, S* ring, volatile int* flag, S* uu) {
+__device__ HT_RQ_ATTR void rq_direction(int m, const S* Cb, int LDC, S* ring, volatile int* flag, S* uu) {
     using CF = RQCfg<S, MAXM>;
     constexpr int LPR = CF::LPR, E = CF::E, SB = CF::SB, NSB = CF::NSB, NA = CF::NA, PLD = CF::PLD;
     constexpr int EP = NSB * SB;  // padded elements per thread

@@ -345,8 +345,15 @@ __device__ __forceinline__ void rqw_apply(S (&val)[RQW<S, MAXM, NW>::RPL][RQW<S,
 // Called by threads [0, NW*32) of the CTA (all of them together; named barrier 1).  Cb: m x m
 // block (col-major, ld LDC); hb/HLD: work storage (see above); uu: output (m entries, written by
 // warp 0); the caller synchronises before reading uu.
+#ifndef HT_RQW_INLINE
+#define HT_RQW_ATTR __noinline__
+#else
+#define HT_RQW_ATTR __forceinline__
+#endif
+// (not inlined: inside the chase kernel the caller's live state pushed this function into spills;
+// as a call, the caller's registers are saved once around it and the RQ gets the register file)
 template <typename S, int MAXM, int NW>
-__device__ __forceinline__ void rq_direction_w(int m, const S* Cb, int LDC, S* hb, int HLD,
+__device__ HT_RQW_ATTR void rq_direction_w(int m, const S* Cb, int LDC, S* hb, int HLD,
                                                uint64_t* bars, int par, S* uu) {
     using CF = RQW<S, MAXM, NW>;
     constexpr int RPW = CF::RPW, RPL = CF::RPL, CPT = CF::CPT, CPL = CF::CPL;
