@@ -529,7 +529,10 @@ __host__ __device__ constexpr bool rq_warp_rows() {
 #ifdef HT_RQW_OFF
     return false;
 #else
-    return sizeof(S) == 8 && MAXM >= 128;
+#ifndef HT_RQW_MIN
+#define HT_RQW_MIN 128
+#endif
+    return sizeof(S) == 8 && MAXM >= HT_RQW_MIN;
 #endif
 }
 
