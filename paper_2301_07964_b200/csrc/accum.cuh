@@ -182,3 +182,101 @@ __global__ void __launch_bounds__(NT) merge_kernel(MergeArgs<S> a) {
         for (int c = tid % 32; c < a.LDB; c += 32)
             Out[(size_t)l * a.LDB + c] = (l < W && c < W) ? M[(size_t)l * LM + c] : S(0.0);
 }
+
+// ---------------------------------------------------------------------------------------
+// K2w: the window blocks in compact WY form for the apply chains ("compact WY
+// representation", "Form compact WY").  The window's reflectors
+// in sweep order, H_t = I - tau_t y_t y_t^* with y_t = v_t at window offset t (m_t entries), give
+// H_0 H_1 ... H_{qp-1} = I - Y T Y^* (forward, columnwise xLARFT: T(t,t) = tau_t,
+// T(s,t) = -tau_t sum_{l=s}^{t-1} T(s,l) (y_l^* y_t)).  Stored per window (chain_wy_stride):
+// Y (WP x (QP + 8), row-major, zero outside the staircase) then T Y^* (QP x (WP + 8)).
+// Grid (K, 2): block (k, 0) from the left reflectors (U_k), (k, 1) from the right ones (V_k).
+template <typename S>
+struct AccumWYArgs {
+    int n, r, qp, j1, K, WP, QP;
+    const S* Qr;
+    const S* Zr;
+    S* U;
+    S* V;
+    const unsigned long long* gate;
+};
+
+template <typename S>
+__host__ __device__ inline size_t accum_wy_smem_bytes(int r, int qp, int QP) {
+    return ((size_t)qp * (r + 1) + 2 * (size_t)QP * (QP + 1)) * sizeof(S);
+}
+
+template <typename S, int NT>
+__global__ void __launch_bounds__(NT) accum_wy_kernel(AccumWYArgs<S> a) {
+    if (input_rejected(a.gate)) return;
+    extern __shared__ __align__(16) unsigned char smraw[];
+    const int n = a.n, r = a.r, qp = a.qp, j1 = a.j1, K = a.K, WP = a.WP, QP = a.QP;
+    const int LDY = QP + 8, LDB = WP + 8;
+    const int k = blockIdx.x;
+    const bool isV = blockIdx.y != 0;
+    const S* R = isV ? a.Zr : a.Qr;
+    S* Out = (isV ? a.V : a.U) + (size_t)k * ((size_t)WP * LDY + (size_t)QP * LDB);
+    const int w = qp + r - 1;
+    const int wk = min(w, n - (j1 + k * r + 1) + 1);
+    S* recs = reinterpret_cast<S*>(smraw);       // qp records (r + 1)
+    S* G = recs + (size_t)qp * (r + 1);          // QP x (QP+1): y_l^* y_t (l < t)
+    S* T = G + (size_t)QP * (QP + 1);            // QP x (QP+1)
+    const int tid = threadIdx.x;
+    for (int t = tid / 32; t < qp; t += NT / 32)
+        for (int c = tid % 32; c <= r; c += 32) recs[(size_t)t * (r + 1) + c] = R[((size_t)t * K + k) * (r + 1) + c];
+    __syncthreads();
+    auto msz = [&](int t) { return min(r, min(n - (j1 + t + k * r), wk - t)); };  // entries of y_t in the window
+    auto tau = [&](int t) { return recs[(size_t)t * (r + 1) + r]; };
+    // Y (row-major), zero outside the staircase and the padding
+    for (int e = tid; e < WP * LDY; e += NT) {
+        const int i = e / LDY, t = e % LDY;
+        S v = S(0.0);
+        if (t < qp && i < wk && i >= t && i - t < msz(t) && !is_zero(tau(t))) v = recs[(size_t)t * (r + 1) + (i - t)];
+        Out[e] = v;
+    }
+    // Gram entries G(l, t) = y_l^* y_t, l < t (rows t .. l + m_l - 1 overlap)
+    for (int e = tid; e < qp * qp; e += NT) {
+        const int l = e / qp, t = e % qp;
+        S g = S(0.0);
+        if (l < t && !is_zero(tau(l)) && !is_zero(tau(t))) {
+            const S* yl = recs + (size_t)l * (r + 1);
+            const S* yt = recs + (size_t)t * (r + 1);
+            const int hi = min(l + msz(l), t + msz(t));
+            for (int i = t; i < hi; ++i) g += conj_mul(yl[i - l], yt[i - t]);
+        }
+        G[(size_t)l * (QP + 1) + t] = g;
+    }
+    __syncthreads();
+    // T rows are independent given G: T(s, t) = -tau_t sum_{l=s}^{t-1} T(s, l) G(l, t)
+    for (int s2 = tid; s2 < QP; s2 += NT) {
+        S* Ts = T + (size_t)s2 * (QP + 1);
+        for (int t = 0; t < QP; ++t) {
+            S v = S(0.0);
+            if (s2 < qp && t < qp) {
+                const S tt = tau(t);
+                if (t == s2) {
+                    v = tt;
+                } else if (t > s2 && !is_zero(tt)) {
+                    S acc = S(0.0);
+                    for (int l = s2; l < t; ++l) acc += Ts[l] * G[(size_t)l * (QP + 1) + t];
+                    v = -(tt * acc);
+                }
+            }
+            Ts[t] = v;
+        }
+    }
+    __syncthreads();
+    // T Y^* (QP x LDB): row s, column c = sum_{t >= s} T(s, t) conj(Y(c, t))
+    S* Bw = Out + (size_t)WP * LDY;
+    for (int e = tid; e < QP * LDB; e += NT) {
+        const int s2 = e / LDB, c = e % LDB;
+        S v = S(0.0);
+        if (s2 < qp && c < wk) {
+            const int tlo = max(s2, c - r + 1), thi = min(qp - 1, c);  // y_t covers rows t .. t + m_t - 1
+            for (int t = tlo; t <= thi; ++t)
+                if (c - t < msz(t) && !is_zero(tau(t)))
+                    v += T[(size_t)s2 * (QP + 1) + t] * conjv(recs[(size_t)t * (r + 1) + (c - t)]);
+        }
+        Bw[e] = v;
+    }
+}

@@ -53,7 +53,18 @@ struct ChainParams {
     int prof_tile;    // the profiled tile of job 0 (HT_CHAIN_PROF_TILE)
     int stair_first;  // right chains: staircase-band tiles dispatched first (HT_STAIR_FIRST=0: off)
     const unsigned long long* gate;  // input-check verdict (input_rejected)
+    // WY blocks ("compact WY"): each window's block
+    // is I - Y T Y^* (forward xLARFT over the window's q reflectors) stored as Y (WP x (QP + 8),
+    // row-major) followed by T Y^* (QP x (WP + 8)); a step is X <- X - (X Y)(T Y^*): 2 w q MACs per
+    // tile row instead of w^2 (real fp64, single windows; wy = 0: dense blocks)
+    int wy;
+    int QP;  // q rounded up to 16
 };
+
+__host__ __device__ constexpr int chain_wy_ldy(int QP) { return QP + 8; }
+__host__ __device__ constexpr size_t chain_wy_stride(int WP, int QP) {  // scalars per window in WY layout
+    return (size_t)WP * chain_wy_ldy(QP) + (size_t)QP * (WP + 8);
+}
 
 // H/T chains are latency-bound by their longest tiles (right updates: the top row tiles walk
 // every window; left updates: the rightmost column tiles).  With spread = G (the SM count) the
@@ -96,10 +107,11 @@ __host__ __device__ constexpr int chain_nt(int WP) { return 32 * chain_wn(WP) * 
 
 // dynamic smem: [64 B mbarriers][circular X: (w+r) x CH_LDX][block ring][staircase refl.]
 template <typename S, int WP>
-__host__ __device__ constexpr size_t chain_smem_bytes(int r, int q, int P = 1) {
+__host__ __device__ constexpr size_t chain_smem_bytes(int r, int q, int P = 1, int QP = 0) {
     return 64 + (size_t)(P > 1 ? q + 2 * P * r - 1 : q + r - 1 + r) * CH_LDX * sizeof(S) +
            (size_t)CH_STAGES * CH_KC * chain_ldb(WP) * sizeof(S) + (size_t)(q + 1) * (r + 1) * sizeof(S) +
-           (size_t)2 * ((q + CH_SBZ - 1) / CH_SBZ) * CH_SBZ * CH_SBZ * sizeof(S);  // staircase block factors
+           (size_t)2 * ((q + CH_SBZ - 1) / CH_SBZ) * CH_SBZ * CH_SBZ * sizeof(S) +  // staircase block factors
+           (size_t)QP * CH_LDX * sizeof(S);  // WY: the tile's X Y (QP columns)
 }
 
 // ---- PTX helpers ---------------------------------------------------------------------
@@ -227,6 +239,10 @@ __device__ __forceinline__ bool chain_tile(const ChainParams<S>& P, int bid, uns
     S* X = reinterpret_cast<S*>(smraw + 64);
     S* ring = X + (size_t)CIRC * CH_LDX;
     S* zsm = ring + (size_t)CH_STAGES * CH_KC * LDB;
+    // WY: the tile's A = X Y (QP columns x CH_LDX), after the staircase records and factors
+    const bool WYm = P.wy != 0;
+    const int QPw = P.QP, LDY = chain_wy_ldy(P.QP);
+    S* Abuf = zsm + (size_t)(qp + 1) * (r + 1) + (size_t)2 * ((qp + CH_SBZ - 1) / CH_SBZ) * CH_SBZ * CH_SBZ;
 
     // ---- window range of this tile ----
     auto rowmax = [&](int k) {  // last row touched by window k in the apply phase (H, T right)
@@ -261,6 +277,7 @@ __device__ __forceinline__ bool chain_tile(const ChainParams<S>& P, int bid, uns
         return full ? glo : khi;
     };
     auto step_blk = [&](int khi, int klo) -> const S* {
+        if (WYm) return J.Blk + (size_t)khi * chain_wy_stride(WP, QPw);
         return klo < khi ? J.MBlk + ((size_t)(klo / PM) * WP) * LDB : J.Blk + ((size_t)khi * WP) * LDB;
     };
     auto step_w = [&](int khi, int klo) { return min(qp + (khi - klo + 1) * r - 1, n - (j1 + klo * r + 1) + 1); };
@@ -316,14 +333,34 @@ __device__ __forceinline__ bool chain_tile(const ChainParams<S>& P, int bid, uns
     int pk = kstart, pc = 0;  // top window of the step being issued, next chunk of it
     int pklo = step_lo(kstart);
     unsigned pseq = 0;
+    // chunks per step: dense -- ceil(w / 16) chunks of the block's rows; WY -- ceil(w / 16) chunks of
+    // Y's rows (16 x LDY), then QP / 16 chunks of T Y^* (16 x LDB)
+    auto step_chunks = [&](int khi, int klo) {
+        const int nk = (step_w(khi, klo) + CH_KC - 1) / CH_KC;
+        return WYm ? nk + QPw / CH_KC : nk;
+    };
     auto issue_next = [&]() {
         if (tid != 0 || pk < kend) return;
         const int s = pseq % CH_STAGES;
-        const S* src = step_blk(pk, pklo) + (size_t)pc * CH_KC * LDB;
-        mbar_expect_tx(&bars[s], CH_KC * LDB * sizeof(S));
-        bulk_g2s(ring + (size_t)s * CH_KC * LDB, src, CH_KC * LDB * sizeof(S), &bars[s]);
+        const S* src;
+        unsigned bytes;
+        if (WYm) {
+            const int nk = (step_w(pk, pklo) + CH_KC - 1) / CH_KC;
+            if (pc < nk) {
+                src = step_blk(pk, pklo) + (size_t)pc * CH_KC * LDY;
+                bytes = CH_KC * LDY * sizeof(S);
+            } else {
+                src = step_blk(pk, pklo) + (size_t)WP * LDY + (size_t)(pc - nk) * CH_KC * LDB;
+                bytes = CH_KC * LDB * sizeof(S);
+            }
+        } else {
+            src = step_blk(pk, pklo) + (size_t)pc * CH_KC * LDB;
+            bytes = CH_KC * LDB * sizeof(S);
+        }
+        mbar_expect_tx(&bars[s], bytes);
+        bulk_g2s(ring + (size_t)s * CH_KC * LDB, src, bytes, &bars[s]);
         ++pseq;
-        if (++pc == (step_w(pk, pklo) + CH_KC - 1) / CH_KC) {
+        if (++pc == step_chunks(pk, pklo)) {
             pc = 0;
             pk = pklo - 1;
             if (pk >= kend) pklo = step_lo(pk);
@@ -388,6 +425,68 @@ __device__ __forceinline__ bool chain_tile(const ChainParams<S>& P, int bid, uns
         const int nch = (wk + CH_KC - 1) / CH_KC;
         const int rowb = wm * (CH_BM / WM) + (lane >> 2);
         const int colb = wn * (WP / WN) + (lane >> 2);
+        if (WYm) {
+            // ---- WY step: A = X(:, window) Y (QP = 32 columns, one 8-column slice per warp column),
+            // staged in smem, then acc = A (T Y^*) and X -= acc in the epilogue ----
+            constexpr int KS = CH_KC / 4;
+            Acc<S> a1[MT];
+#pragma unroll
+            for (int mt = 0; mt < MT; ++mt) acc_zero(a1[mt]);
+            const int colq = wn * 8 + (lane >> 2);
+            for (int ch = 0; ch < nch; ++ch) {
+                const int s = cseq % CH_STAGES;
+                mbar_wait(&bars[s], (cseq / CH_STAGES) & 1);
+                gsync();
+                issue_next();
+                const S* Bs = ring + (size_t)s * CH_KC * LDB;
+                S a[KS][MT], b[KS];
+#pragma unroll
+                for (int ks = 0; ks < KS; ++ks) {
+                    const int kl = ch * CH_KC + ks * 4 + (lane & 3);
+                    int pos = p + kl;
+                    if (pos >= CIRC) pos -= CIRC;
+                    if (pos >= CIRC) pos -= CIRC;
+#pragma unroll
+                    for (int mt = 0; mt < MT; ++mt) a[ks][mt] = X[pos * CH_LDX + rowb + mt * 8];
+                    b[ks] = Bs[(ks * 4 + (lane & 3)) * LDY + colq];
+                }
+#pragma unroll
+                for (int ks = 0; ks < KS; ++ks)
+#pragma unroll
+                    for (int mt = 0; mt < MT; ++mt) mma_step(a1[mt], a[ks][mt], b[ks]);
+                ++cseq;
+            }
+#pragma unroll
+            for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) Abuf[(wn * 8 + (lane & 3) * 2 + h) * CH_LDX + rowb + mt * 8] = acc_get(a1[mt], h);
+            gsync();  // A complete
+            for (int ch = 0; ch < QPw / CH_KC; ++ch) {
+                const int s = cseq % CH_STAGES;
+                mbar_wait(&bars[s], (cseq / CH_STAGES) & 1);
+                gsync();
+                issue_next();
+                const S* Bs = ring + (size_t)s * CH_KC * LDB;
+                if (wn * (WP / WN) < wk) {
+                    S a[KS][MT], b[KS][NTL];
+#pragma unroll
+                    for (int ks = 0; ks < KS; ++ks) {
+                        const int kk = ch * CH_KC + ks * 4 + (lane & 3);
+#pragma unroll
+                        for (int mt = 0; mt < MT; ++mt) a[ks][mt] = Abuf[kk * CH_LDX + rowb + mt * 8];
+#pragma unroll
+                        for (int nt = 0; nt < NTL; ++nt) b[ks][nt] = Bs[(ks * 4 + (lane & 3)) * LDB + colb + nt * 8];
+                    }
+#pragma unroll
+                    for (int ks = 0; ks < KS; ++ks)
+#pragma unroll
+                        for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+                            for (int nt = 0; nt < NTL; ++nt) mma_step(acc[mt][nt], a[ks][mt], b[ks][nt]);
+                }
+                ++cseq;
+            }
+        } else
         for (int ch = 0; ch < nch; ++ch) {
             const int s = cseq % CH_STAGES;
             mbar_wait(&bars[s], (cseq / CH_STAGES) & 1);
@@ -437,7 +536,8 @@ __device__ __forceinline__ bool chain_tile(const ChainParams<S>& P, int bid, uns
                     if (upd && col < wk) {
                         int pos = p + col;
                         if (pos >= CIRC) pos -= CIRC;
-                        X[pos * CH_LDX + row] = maybe_conj(acc_get(acc[mt][nt], h), false);
+                        if (WYm) X[pos * CH_LDX + row] -= acc_get(acc[mt][nt], h);  // X - (X Y)(T Y^*)
+                        else X[pos * CH_LDX + row] = maybe_conj(acc_get(acc[mt][nt], h), false);
                     }
                 }
         }

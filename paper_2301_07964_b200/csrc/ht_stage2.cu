@@ -89,11 +89,11 @@ int64_t default_q(int64_t n, int64_t r, int is_complex) {
 }
 
 template <typename S, int WP>
-size_t chain_bytes(int r, int q, int P = 1) { return chain_smem_bytes<S, WP>(r, q, P); }
+size_t chain_bytes(int r, int q, int P = 1, int QP = 0) { return chain_smem_bytes<S, WP>(r, q, P, QP); }
 
 template <typename S, int WP>
 int launch_chain(const ChainParams<S>& P, int grid, int r, int q, cudaStream_t st, size_t min_smem) {
-    const size_t bytes = std::max(chain_bytes<S, WP>(r, q, P.P), min_smem);
+    const size_t bytes = std::max(chain_bytes<S, WP>(r, q, P.P, P.wy ? P.QP : 0), min_smem);
     static bool attr_set = false;  // per instantiation
     if (!attr_set) {
         CK(cudaFuncSetAttribute(chain_kernel<S, WP>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
@@ -121,7 +121,7 @@ int chain(const ChainParams<S>& P, int WP, int grid, int r, int q, cudaStream_t 
 // Q/Z chains as two tile groups per CTA (chain_kernel2): one CTA per SM, 2 x the group bytes
 template <typename S, int WP>
 int launch_chain2(const ChainParams<S>& P, int grid, int r, int q, cudaStream_t st) {
-    const size_t gb = (chain_bytes<S, WP>(r, q, P.P) + 127) / 128 * 128;
+    const size_t gb = (chain_bytes<S, WP>(r, q, P.P, P.wy ? P.QP : 0) + 127) / 128 * 128;
     static bool attr_set = false;
     if (!attr_set) {
         CK(cudaFuncSetAttribute(chain_kernel2<S, WP>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
@@ -166,13 +166,13 @@ int chain_prepare(int WP) {  // smem attribute outside any stream capture
 }
 
 template <typename S>
-size_t chain_bytes_rt(int WP, int r, int q, int P = 1) {
+size_t chain_bytes_rt(int WP, int r, int q, int P = 1, int QP = 0) {
     switch (WP) {
-        case 32: return chain_bytes<S, 32>(r, q, P);
-        case 64: return chain_bytes<S, 64>(r, q, P);
-        case 96: return chain_bytes<S, 96>(r, q, P);
-        case 128: return chain_bytes<S, 128>(r, q, P);
-        case 160: return chain_bytes<S, 160>(r, q, P);
+        case 32: return chain_bytes<S, 32>(r, q, P, QP);
+        case 64: return chain_bytes<S, 64>(r, q, P, QP);
+        case 96: return chain_bytes<S, 96>(r, q, P, QP);
+        case 128: return chain_bytes<S, 128>(r, q, P, QP);
+        case 160: return chain_bytes<S, 160>(r, q, P, QP);
         default: return (size_t)1 << 40;
     }
 }
@@ -258,13 +258,14 @@ struct Plan {
     bool qz_late = true;   // Q/Z chains of a group start after its H/T chains (HT_QZ_LATE=0: after K2)
     bool qz_groups = false;  // Q/Z chains as two tile groups per CTA (chain_kernel2; HT_QZ_GROUPS=0: off)
     bool far_side = false;   // one GPU: far H/T tiles' right updates on the side stream (HT_FAR_SIDE)
+    int wy = 0, QP = 0;      // WY window blocks (chain.cuh ChainParams::wy; accum_wy_kernel)
     int hlag = 1;          // helper row split (ChaseArgs::hlag): 0 for r >= 32 (HT_HELPER_LAG overrides)
     size_t mrg_bytes = 0;
     const unsigned long long* gate = nullptr;  // device verdict words of the input check (nullptr: none)
     bool is_root() const { return comm == nullptr || rank == root; }
     bool qz() const { return Q || Z; }
     bool same(const Plan& o) const {
-        return n == o.n && r == o.r && q == o.q && strip_cap == o.strip_cap && helpers == o.helpers && P == o.P && qz_late == o.qz_late && qz_groups == o.qz_groups && far_side == o.far_side && hlag == o.hlag && G == o.G && emul_ht == o.emul_ht && gate == o.gate && H == o.H && ldh == o.ldh &&
+        return n == o.n && r == o.r && q == o.q && strip_cap == o.strip_cap && helpers == o.helpers && P == o.P && qz_late == o.qz_late && qz_groups == o.qz_groups && far_side == o.far_side && wy == o.wy && hlag == o.hlag && G == o.G && emul_ht == o.emul_ht && gate == o.gate && H == o.H && ldh == o.ldh &&
                T == o.T && ldt == o.ldt && Q == o.Q && ldq == o.ldq && Z == o.Z && ldz == o.ldz;
     }
 };
@@ -556,7 +557,12 @@ int enqueue_groups(const Plan<S>& p, Workspace<S>& ws, cudaStream_t stream, bool
         if (qz && g >= NUV) CK(cudaStreamWaitEvent(stream, ws.ev_qz[bsel], 0));  // Q/Z of g-NUV done with U/V[bsel]
         AccumArgs<S> aa{n, r, qp, j1, K, WP, LDB, p.acc_bytes >= accum_smem_bytes<S>(r, q, true) ? 1 : 0, ws.Qr, ws.Zr,
                         ws.U[bsel], ws.V[bsel], p.gate};
-        if (root || qz || p.shard_ht()) {
+        if (p.wy && (root || qz || p.shard_ht())) {
+            AccumWYArgs<S> aw{n, r, qp, j1, K, WP, p.QP, ws.Qr, ws.Zr, ws.U[bsel], ws.V[bsel], p.gate};
+            accum_wy_kernel<S, ACC_NT><<<dim3(K, 2), ACC_NT, accum_wy_smem_bytes<S>(r, q, p.QP), stream>>>(aw);
+            CK(cudaGetLastError());
+            g_last_launches += 1;
+        } else if (root || qz || p.shard_ht()) {
             accum_kernel<S, ACC_NT><<<dim3(K, 2), ACC_NT, p.acc_bytes, stream>>>(aa);
             CK(cudaGetLastError());
             g_last_launches += 2;
@@ -580,6 +586,8 @@ int enqueue_groups(const Plan<S>& p, Workspace<S>& ws, cudaStream_t stream, bool
             ChainParams<S> pf{n, r, qp, j1, K, {{p.H, p.ldh, ws.V[bsel], ws.MV[bsel], CM_AB_RIGHT, 0, nf, 0},
                                                 {p.T, p.ldt, ws.V[bsel], ws.MV[bsel], CM_AB_RIGHT, 0, nf, 0}}, 2, ws.Zr, p.P, 0};
             pf.gate = p.gate;
+            pf.wy = p.wy;
+            pf.QP = p.QP;
             if (p.qz_groups) {
                 if (int rc = chain2<S>(pf, WP, std::min(nf, p.qz_ctas), r, q, ws.side)) return rc;
             } else if (int rc = chain<S>(pf, WP, std::min(2 * nf, p.qz_ctas), r, q, ws.side, 116 * 1024)) {
@@ -603,6 +611,8 @@ int enqueue_groups(const Plan<S>& p, Workspace<S>& ws, cudaStream_t stream, bool
                                                     {Tk, ltk, ws.V[bsel], ws.MV[bsel], CM_AB_RIGHT, 0, cnt, rk, p.G}}, 2, ws.Zr, p.P,
                                   0};
                 pf.gate = p.gate;
+            pf.wy = p.wy;
+            pf.QP = p.QP;
                 if (int rc = chain<S>(pf, WP, 2 * cnt, r, q, stream)) return rc;
                 ++g_last_launches;
             }
@@ -613,12 +623,16 @@ int enqueue_groups(const Plan<S>& p, Workspace<S>& ws, cudaStream_t stream, bool
                               getenv("HT_CHAIN_PROF_TILE") ? atoi(getenv("HT_CHAIN_PROF_TILE")) : 0,
                               !(getenv("HT_STAIR_FIRST") && atoi(getenv("HT_STAIR_FIRST")) == 0)};
             pr.gate = p.gate;
+            pr.wy = p.wy;
+            pr.QP = p.QP;
             if (int rc = chain<S>(pr, WP, 2 * (tiles - nf), r, q, stream)) return rc;
             ChainParams<S> pl{n, r, qp, j1, K, {{p.H, p.ldh, ws.U[bsel], ws.MU[bsel], CM_A_LEFT, 1, tiles, 0},
                                                 {p.T, p.ldt, ws.U[bsel], ws.MU[bsel], CM_B_LEFT, 1, tiles, 0}}, 2, ws.Zr, p.P,
                               chain_spread(p.nsm), ws.k1prof ? ws.k1prof + 24 : nullptr,
                               getenv("HT_CHAIN_PROF_TILE") ? atoi(getenv("HT_CHAIN_PROF_TILE")) : 0};
             pl.gate = p.gate;
+            pl.wy = p.wy;
+            pl.QP = p.QP;
             if (int rc = chain<S>(pl, WP, 2 * tiles, r, q, stream)) return rc;
             g_last_launches += 2;
         }
@@ -639,6 +653,8 @@ int enqueue_groups(const Plan<S>& p, Workspace<S>& ws, cudaStream_t stream, bool
                                                     {p.Z, p.ldz, ws.V[bsel], ws.MV[bsel], CM_PLAIN, 0, nt, t0}},
                                   (p.Q && p.Z) ? 2 : 1, ws.Zr, p.P};
                 pq.gate = p.gate;
+            pq.wy = p.wy;
+            pq.QP = p.QP;
                 // persistent grid leaving q whole SMs: the chase of the next group starts at once
                 if (p.qz_groups) {
                     if (int rc = chain2<S>(pq, WP, std::min((pq.njobs * nt + 1) / 2, p.qz_ctas), r, q, ws.side)) return rc;
@@ -913,7 +929,18 @@ int run(int64_t n64, int64_t r64, S* H, int64_t ldh, S* T, int64_t ldt, S* Q, in
     const size_t acc_bytes = accum_smem_bytes<S>(r, q, acc_pre);
     const void* chase_fn = chase_kernel_for<S>(r);
     if (!chase_fn || q > 148) return refuse(HT_EUNSUPPORTED);  // one co-resident CTA per sweep
-    const size_t ch_bytes = chain_bytes_rt<S>(WP, r, q, PM);
+    // WY window blocks: real fp64, q in (16, 32] (QP = 32), single windows (no
+    // K2m), 4 warp columns.  A step costs 2 w QP MACs per tile row instead of w^2 (w = q + r - 1), but
+    // runs two GEMMs with a shared-memory hand-off: measured config 5 (w = 159) 103.1 -> 95.8 s per
+    // call, config 4 (w = 95) 10.88 -> 12.47 s -- on for r >= 128 (HT_WY=0/1 overrides)
+    int wy = 0;
+    {
+        const bool feasible = sizeof(S) == 8 && PM == 1 && q > 16 && q <= 32 && chain_wn(WP) == 4;
+        const char* e = getenv("HT_WY");
+        wy = feasible && (e ? atoi(e) != 0 : r >= 128);
+    }
+    const int QPw = wy ? 32 : 0;
+    const size_t ch_bytes = chain_bytes_rt<S>(WP, r, q, PM, QPw);
     const size_t mrg_bytes = PM > 1 ? merge_smem_bytes<S>(Wm, w) : 0;
     int dev = 0, smem_optin = 0, nsm = 0;
     CK(cudaGetDevice(&dev));
@@ -925,6 +952,9 @@ int run(int64_t n64, int64_t r64, S* H, int64_t ldh, S* T, int64_t ldt, S* Q, in
     if (PM > 1) CK(cudaFuncSetAttribute(merge_kernel<S, ACC_NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mrg_bytes));
     CK(cudaFuncSetAttribute(chase_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)chase_bytes));
     CK(cudaFuncSetAttribute(accum_kernel<S, ACC_NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)acc_bytes));
+    if (wy)
+        CK(cudaFuncSetAttribute(accum_wy_kernel<S, ACC_NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)accum_wy_smem_bytes<S>(r, q, QPw)));
 
     if (int rcp = chain_prepare<S>(WP)) return refuse(rcp);
     // far-strip helpers per sweep: as many as fit next to the q sweeps, at most 3 (HT_HELPERS)
@@ -934,6 +964,8 @@ int run(int64_t n64, int64_t r64, S* H, int64_t ldh, S* T, int64_t ldt, S* Q, in
     Plan<S> pl{n, r, q, WP, LDB, Kmax, strip_cap, chase_bytes, acc_bytes, chase_fn, H, ldh, T, ldt, Q, ldq, Z, ldz,
                std::max(8, nsm - (1 + helpers) * q)};
     pl.helpers = helpers;
+    pl.wy = wy;
+    pl.QP = QPw;
     pl.P = PM;
     pl.nsm = nsm;
     pl.hlag = getenv("HT_HELPER_LAG") ? (atoi(getenv("HT_HELPER_LAG")) == 0 ? 0 : 1) : (r >= 32 ? 0 : 1);
