@@ -19,6 +19,7 @@
 #pragma once
 #include "scalar.cuh"
 #include "rqw.cuh"
+#include "rqu.cuh"
 
 #ifndef IDX
 #define IDX(p, ld, i, j) (p)[((int64_t)(i) - 1) + ((int64_t)(j) - 1) * (int64_t)(ld)]
@@ -51,6 +52,19 @@ struct ChaseArgs {
     // [start, end] pairs -- sweeps at trace[(t K + k) 2 + 0/1], helpers after qp K pairs at
     // trace[(qp K + (t H + h) K + k) 2 + 0/1]; checked on the host (ht_stage2.cu, check_lag)
     unsigned long long* trace;
+    // RQ update (rqu.cuh, real r in (32, 64]): the hand-over of sweep j to sweep j+1 per window k,
+    // R~(2:m,2:m) then (Q~ Z)(2:m,2:m), each row-major with ld MAXM, at Fg + k fst
+    double* Fg = nullptr;
+    int64_t fst = 0;
+    int rqu = 0;        // 0: Householder RQ per step; 1: RQ update in the sweep; 2: direction by a
+                        // triangular solve, the RQ update (hand-over) by the sweep's helper h = k mod H
+    double* Fb = nullptr;  // rqu 2: the caught-up column b of step (j,k) per k (MAXM each)
+    int* Fdone = nullptr;  // rqu 2: per k, j+1 once the hand-over of sweep j's step k is in Fg
+};
+
+// shared-memory buffers of the RQ update (chase_kernel carves them; helpers use them too)
+struct RQUBufs {
+    double *Rs, *Qs, *wpart, *cs1, *cs2, *xs, *v, *z, *uu;
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -556,8 +570,15 @@ __host__ __device__ constexpr bool chase_dense_catchup(int r) {
     return r <= 64 && r * (int)sizeof(S) <= 256;
 }
 
+// K1's RQ-update path (rqu.cuh): real fp64, 32 < r <= 64 (MAXM = 64)
+template <typename S, int MAXM>
+__host__ __device__ constexpr bool rqu_supported() { return sizeof(S) == 8 && MAXM == 64; }
 template <typename S>
-__host__ __device__ inline size_t chase_smem_elems(int r, int qp, int strip_cap) {
+__host__ __device__ inline bool rqu_supported_r(int r) { return sizeof(S) == 8 && r > 32 && r <= 64; }
+constexpr int CHASE_NT_RQU = 256;
+
+template <typename S>
+__host__ __device__ inline size_t chase_smem_elems(int r, int qp, int strip_cap, bool rqu = false) {
     const int w = qp + r - 1;
     const size_t XL = (size_t)(w + r + 8);
     const bool overlay = r > 64;         // the RQ ring (r slots of 132 for MAXM = 128) overlays the B block
@@ -571,6 +592,7 @@ __host__ __device__ inline size_t chase_smem_elems(int r, int qp, int strip_cap)
            5 * (size_t)(qp + 8) +        // WY temporaries
            (overlay ? 0 : XL + (size_t)r * (r + 1) + (size_t)qp * (r + 1) + (size_t)qp * (qp + 1)) +  // prefetch set
            (chase_dense_catchup<S>(r) ? 2 * (size_t)w * (w | 1) + 2 * (size_t)(w + 1) : 0) +  // M_t, M_t(k+1), tmp
+           (rqu ? RQUCfg<CHASE_NT_RQU, 64>::extra : 0) +  // RQ update: Q0, w parts, rotations
            (size_t)strip_cap * (r + 1);  // staged strip rows
 }
 
@@ -587,7 +609,7 @@ __host__ __device__ inline size_t chase_smem_elems(int r, int qp, int strip_cap)
 // being prefetched during step k-2 (the B block's last column is patched from the caught-up y
 // anyway); sweep j itself never reads those rows again.
 template <typename S, int NT, int MAXM>
-__device__ __forceinline__ void far_strip_helper(const ChaseArgs<S>& a, int t, int h, S* sm) {
+__device__ __forceinline__ void far_strip_helper(const ChaseArgs<S>& a, int t, int h, S* sm, const RQUBufs& rb) {
     const int H = a.helpers;
     constexpr int RB = 64;  // row block: helper h owns blocks h, h+H, ... (relative to j1)
     const int n = a.n, r = a.r, qp = a.qp, j1 = a.j1, K = a.K;
@@ -683,6 +705,44 @@ __device__ __forceinline__ void far_strip_helper(const ChaseArgs<S>& a, int t, i
             if (a.trace) a.trace[((int64_t)qp * K + ((int64_t)t * H + h) * K + k) * 2 + 1] = gtimer();
             st_release(&hprog[t * H + h], k + 1);
         }
+        if constexpr (rqu_supported<S, MAXM>()) {
+            // rqu 2: the RQ update of step (j,k) and its hand-over to sweep j+1 (rqu.cuh), unless the
+            // sweep fell back to doing it itself; sweep j+1 waits for Fdone[k] = j+1 at its step k
+            const int jb = j + max(0, (k - 1) * r + 1);
+            if (a.rqu == 2 && k % H == h && m >= 2 && jb <= n && ld_acquire(&a.Fdone[k]) < j + 1) {
+                constexpr int RLD = RQUCfg<NT, MAXM>::RLD;
+                const bool hasB = i1 + r - 1 <= n;
+                const int f = hasB ? m - 1 : m;
+                double* FR = a.Fg + (int64_t)k * a.fst;
+                double* FW = FR + MAXM * MAXM;
+                for (int e = tid; e < f * f; e += NT) {
+                    const int p = e / f, c = e - p * f;
+                    rb.Qs[p * RLD + c] = ldcg(FW + p * MAXM + c);
+                    if (c >= p) rb.Rs[p * RLD + c] = ldcg(FR + p * MAXM + c);
+                }
+                if (hasB)
+                    for (int i = tid; i < m; i += NT) {
+                        rb.Rs[i * RLD + (m - 1)] = ldcg(a.Fb + (int64_t)k * MAXM + i);
+                        rb.Qs[(m - 1) * RLD + i] = (i == m - 1) ? 1.0 : 0.0;
+                        rb.Qs[i * RLD + (m - 1)] = (i == m - 1) ? 1.0 : 0.0;
+                    }
+                const double* qrec = reinterpret_cast<const double*>(a.Qr + ((int64_t)t * K + k) * (r + 1));
+                const double* zrec = reinterpret_cast<const double*>(a.Zr + ((int64_t)t * K + k) * (r + 1));
+                for (int c = tid; c < m; c += NT) {
+                    rb.v[c] = ldcg(qrec + c);
+                    rb.z[c] = ldcg(zrec + c);
+                }
+                const double tau = ldcg(qrec + r), sig = ldcg(zrec + r);
+                __syncthreads();
+                rqu_direction<NT, MAXM>(m, rb.v, tau, rb.Rs, rb.Qs, rb.wpart, rb.cs1, rb.cs2, rb.uu);
+                rqu_handoff<NT, MAXM>(m, rb.Rs, rb.Qs, rb.z, sig, FR, FW);
+                __syncthreads();
+                if (tid == 0) {
+                    __threadfence();
+                    st_release(&a.Fdone[k], j + 1);
+                }
+            }
+        }
         if (a.prof && tid == 0) {
             const long long now = clock64();
             hx += now - tc;
@@ -744,7 +804,22 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
     S* Msm0 = PF ? Tsm1 + (size_t)qp * TL : ys1;  // M_t(k), even / odd steps (L x L, ld MLD)
     S* Msm1 = MK ? Msm0 + (size_t)w * MLD : Msm0;
     S* mtmp = MK ? Msm1 + (size_t)w * MLD : Msm0;  // 2 (w+1): catch-up outputs / M update row
-    S* strip = MK ? mtmp + 2 * (size_t)(w + 1) : Msm0;  // strip_cap rows x (r+1) (row-major)
+    S* strip0 = MK ? mtmp + 2 * (size_t)(w + 1) : Msm0;
+    // RQ update (rqu.cuh): R0 overlays the RQ ring, Q0 / w parts / rotations before the strip
+    constexpr bool RQU_OK = rqu_supported<S, MAXM>();
+    const bool rqu = RQU_OK && a.rqu != 0;
+    using RQC = RQUCfg<NT, (RQU_OK ? MAXM : 64)>;
+    constexpr int RLD = RQC::RLD;
+    double* const Rs = reinterpret_cast<double*>(ring);
+    double* const Qs = reinterpret_cast<double*>(strip0);
+    double* const wpart = Qs + (size_t)RQC::RLD * (RQU_OK ? MAXM : 64);
+    double* const cs1 = wpart + (size_t)RQC::NPART * (RQU_OK ? MAXM : 64);
+    double* const cs2 = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(cs1 + 2 * (RQU_OK ? MAXM : 64)) + 15) & ~(uintptr_t)15);
+    double* const xs = cs2 + 2 * (RQU_OK ? MAXM : 64);
+    __shared__ int rqu_ok;
+    if (rqu)
+        for (int i = threadIdx.x; i < (RQU_OK ? MAXM : 64); i += NT) cs2[2 * i] = RQU_SENTINEL;
+    S* strip = rqu ? strip0 + RQC::extra : strip0;  // strip_cap rows x (r+1) (row-major)
     const int LDC = r + 1;
     // sweep index by ticket (not blockIdx): a CTA only ever waits on a sweep whose CTA already
     // started, so a normal (non-cooperative) launch cannot deadlock when SMs are shared
@@ -755,7 +830,9 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
     const int t = t_sh / (1 + a.helpers);
     if (t >= qp) return;
     if (role > 0) {
-        far_strip_helper<S, NT, MAXM>(a, t, role - 1, sm);
+        far_strip_helper<S, NT, MAXM>(a, t, role - 1, sm,
+                                      RQUBufs{Rs, Qs, wpart, cs1, cs2, xs, reinterpret_cast<double*>(vq),
+                                              reinterpret_cast<double*>(vz), reinterpret_cast<double*>(uu)});
         return;
     }
     int* hprog = a.prog + qp + 1;
@@ -763,15 +840,33 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
     const int kcount = min(K, 2 + (n - j - 1) / r);
     const int kprev = (t > 0) ? min(K, 2 + (n - j) / r) : 0;
     int cur = 0;
-    long long pt[16] = {};
-    long long tc = clock64();
-    // (the shared load makes a preceding barrier's deferred block land before the clock read)
+    // K1 profile (HT_K1PROF): thread 0's cycle counts per phase, in shared memory (a register array
+    // cost ~48 registers in every build)
+    __shared__ long long pt[24];
+    __shared__ long long tc;
+    if (tid == 0) {
+        for (int i = 0; i < 24; ++i) pt[i] = 0;
+        tc = clock64();
+    }
 #define K1_TICK(slot)                         \
     do {                                      \
-        if (a.prof) (void)*(volatile int*)&t_sh; \
-        const long long now_ = clock64();     \
-        pt[slot] += now_ - tc;                \
-        tc = now_;                            \
+        if (a.prof && tid == 0) {             \
+            (void)*(volatile int*)&t_sh;      \
+            const long long now_ = clock64(); \
+            pt[slot] += now_ - tc;            \
+            tc = now_;                        \
+        }                                     \
+    } while (0)
+    // sub-phase slot (16..23) that is also counted in its parent slot
+#define K1_SUB(slot, parent)                  \
+    do {                                      \
+        if (a.prof && tid == 0) {             \
+            (void)*(volatile int*)&t_sh;      \
+            const long long now_ = clock64(); \
+            pt[slot] += now_ - tc;            \
+            pt[parent] += now_ - tc;          \
+            tc = now_;                        \
+        }                                     \
     } while (0)
     // cp.async of step kk's y column, catch-up records, T factor and B block into a buffer set
     auto issue_step_loads = [&](int kk, S* ysb, S* Cbb, S* recb, S* Tsmb, S* Mb, int th0, int nth, bool with_y) {
@@ -803,6 +898,7 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
     };
     bool pf_next = false;  // step k's loads were issued during step k-1
     for (int k = 0; k < kcount; ++k) {
+        bool rqu_fallback = false;  // rqu 2: the solve failed, the sweep did the RQ update itself
         const bool have = pf_next;
         pf_next = false;
         if (t > 0) {
@@ -815,10 +911,15 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
                 int v = ld_relaxed(&a.prog[t - 1]);
                 int hv[3] = {hneed, hneed, hneed};
                 for (int h = 0; h < a.helpers && h < 3; ++h) hv[h] = ld_relaxed(hp + h);
+                // rqu 2: sweep j-1's hand-over for window k (its helper's RQ update)
+                const bool fw = RQU_OK && a.rqu == 2 && min(j + (k + 1) * r, n) - (j + k * r + 1) >= 1 &&
+                                j + max(0, (k - 1) * r + 1) <= n;
+                int fv = fw ? ld_relaxed(&a.Fdone[k]) : j;
                 while (v < need) v = ld_relaxed(&a.prog[t - 1]);
                 K1_TICK(0);
                 for (int h = 0; h < a.helpers && h < 3; ++h)
                     while (hv[h] < hneed) hv[h] = ld_relaxed(hp + h);
+                while (fv < j) fv = ld_relaxed(&a.Fdone[k]);
                 asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
                 K1_TICK(9);
             }
@@ -882,6 +983,21 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
         else k1_wait_group<1>();
         __syncthreads();
         K1_TICK(1);
+        if constexpr (RQU_OK) {
+            if (rqu) {  // sweep j-1's hand-over for window k (rqu.cuh), waited for before the RQ update
+                if (gen && j > 1) {
+                    const int f = hasB ? m - 1 : m;
+                    const double* FR = a.Fg + (int64_t)k * a.fst;
+                    const double* FW = FR + MAXM * MAXM;
+                    for (int e = tid; e < f * f; e += NT) {
+                        const int p = e / f, c = e - p * f;
+                        k1_ld(&Qs[p * RLD + c], FW + p * MAXM + c);
+                        if (c >= p) k1_ld(&Rs[p * RLD + c], FR + p * MAXM + c);
+                    }
+                }
+                k1_commit();
+            }
+        }
         if (jb <= n && nx > 0) {
             // ---- (S2) catch-up in WY form: x(0:L) <- x - Y T^* Y^* x (same for y) ----------------
             // (dense path with a reflector: merged with S3 below)
@@ -1055,6 +1171,34 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
                     S* qr = a.Qr + ((int64_t)t * K + k) * (r + 1);
                     for (int c = tid; c < m; c += NT) qr[c] = vq[c];
                     if (tid == 0) qr[r] = tau;
+                    if constexpr (RQU_OK) {
+                        if (rqu) {  // R0 / Q0 from B0 (still unreduced in Cb): see rqu.cuh
+                            if (j == 1) {  // T itself: R0 = B0 (upper triangular), Q0 = I
+                                for (int e = tid; e < m * m; e += NT) {
+                                    const int p = e / m, c = e - p * m;
+                                    Qs[p * RLD + c] = (p == c) ? 1.0 : 0.0;
+                                    if (c >= p) Rs[p * RLD + c] = re(Cb[p + c * LDC]);
+                                }
+                                if (a.rqu == 2) {  // the helper reads the hand-over form of it
+                                    const int f = hasB ? m - 1 : m;
+                                    double* FR = a.Fg + (int64_t)k * a.fst;
+                                    for (int e = tid; e < f * f; e += NT) {
+                                        const int p = e / f, c = e - p * f;
+                                        FR[MAXM * MAXM + p * MAXM + c] = (p == c) ? 1.0 : 0.0;
+                                        if (c >= p) FR[p * MAXM + c] = re(Cb[p + c * LDC]);
+                                    }
+                                }
+                            } else if (hasB) {  // last column b = B0(:, m), Q0 = diag(W, 1)
+                                for (int i = tid; i < m; i += NT) {
+                                    Rs[i * RLD + (m - 1)] = re(Cb[i + (m - 1) * LDC]);
+                                    Qs[(m - 1) * RLD + i] = (i == m - 1) ? 1.0 : 0.0;
+                                    Qs[i * RLD + (m - 1)] = (i == m - 1) ? 1.0 : 0.0;
+                                }
+                            }
+                            if (a.rqu == 2 && hasB)  // b for the helper's RQ update
+                                for (int i = tid; i < m; i += NT) a.Fb[(int64_t)k * MAXM + i] = re(Cb[i + (m - 1) * LDC]);
+                        }
+                    }
                 }
                 __syncthreads();
                 K1_TICK(8);
@@ -1115,6 +1259,7 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
                         }
                     }
                 } else if (!MK) {
+                    const long long s4t0 = a.prof ? clock64() : 0;
                     // xLARFT column t: T(0:t,t) = -tau T(0:t,0:t) (Y(:,0:t)^* v), T(t,t) = tau
                     const int hn = NT - NT / 2, me = tid - NT / 2;
                     for (int s = me; s < t; s += hn) {
@@ -1147,7 +1292,9 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
                         }
                         tr[p] = val;
                     }
+                    if (a.prof && tid == NT / 2) atomicAdd((unsigned long long*)&pt[23], (unsigned long long)(clock64() - s4t0));
                 }
+                K1_SUB(22, 3);
                 __syncthreads();
                 if constexpr (OVERLAY) {  // the block goes to HBM: the RQ ring reuses its smem
                     for (int cc = warp; cc < m; cc += NW)
@@ -1156,6 +1303,27 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
                 }
                 K1_TICK(3);
                 // ---- (S5) RQ of the block -> Z_k^j ---------------------------------------------
+                if (rqu) {  // RQ update (rqu.cuh): the next step's prefetch first, then F / strip landed
+                    if (PF && k + 1 < kcount) {
+                        issue_step_loads(k + 1, (k & 1) ? ys0 : ys1, (k & 1) ? Cb0 : Cb1, (k & 1) ? rec0 : rec1,
+                                         (k & 1) ? Tsm0 : Tsm1, (k & 1) ? Msm0 : Msm1, 0, NT, a.hlag != 0);
+                        asm volatile("cp.async.commit_group;\n" ::: "memory");
+                        pf_next = true;
+                    }
+                    if (pf_next) k1_wait_group<1>();
+                    else k1_wait_group<0>();
+                    __syncthreads();
+                    K1_SUB(16, 6);
+                    if constexpr (RQU_OK) {
+                        const double* vd = reinterpret_cast<const double*>(vq);
+                        double* ud = reinterpret_cast<double*>(uu);
+                        if (a.rqu == 2)
+                            rqu_fallback = !rqu_solve<NT, MAXM>(m, vd, re(tau), Rs, Qs, wpart, xs, ud, &rqu_ok,
+                                                                a.prof ? pt : nullptr, &tc);
+                        if (a.rqu != 2 || rqu_fallback)
+                            rqu_direction<NT, MAXM>(m, vd, re(tau), Rs, Qs, wpart, cs1, cs2, ud, a.prof ? pt : nullptr, &tc);
+                    }
+                } else {
                 if (PF && k + 1 < kcount) {  // next step's inputs land while the RQ runs (issued by
                     // the warps the RQ does not use, if any)
                     constexpr int RQT = rq_nthr<S, MAXM>();
@@ -1215,6 +1383,7 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
                 if (tid < rq_nthr<S, MAXM>())
                     rq_dir<S, MAXM>(m, Cb, LDC, ring, &rq_flag, uu, OVERLAY ? 132 : ring_pld(r), rq_bars, rq_calls & 1);
                 ++rq_calls;
+                }
                 if (pf_next) k1_wait_group<1>();  // the strip (the prefetch group may stay in flight)
                 else k1_wait_group<0>();
                 __syncthreads();
@@ -1309,6 +1478,13 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
                 S* zr = a.Zr + ((int64_t)t * K + k) * (r + 1);
                 for (int c = tid; c < m; c += NT) zr[c] = vz[c];
                 if (tid == 0) zr[r] = sig;
+                if constexpr (RQU_OK)
+                    if (rqu && (a.rqu == 1 || rqu_fallback)) {  // hand-over to sweep j+1 (read at its step k)
+                        K1_TICK(5);
+                        double* FR = a.Fg + (int64_t)k * a.fst;
+                        rqu_handoff<NT, MAXM>(m, Rs, Qs, reinterpret_cast<const double*>(vz), re(sig), FR, FR + MAXM * MAXM);
+                        K1_SUB(20, 5);
+                    }
             }
         }
         // the next step's column jb must come from global if this step did not produce it
@@ -1321,13 +1497,15 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
         }
         if (tid == NT - 32) {  // (not thread 0: it spins on the previous sweep meanwhile)
             __threadfence();
+            if (RQU_OK && rqu_fallback) st_release(&a.Fdone[k], j + 1);  // (rqu 2: the sweep did the hand-over)
             if (a.trace) a.trace[((int64_t)t * K + k) * 2 + 1] = gtimer();
             st_release(&a.prog[t], k + 1);
         }
         cur ^= 1;
-        pt[11] += 1;  // step count (not a time slot)
+        if (tid == 0) pt[11] += 1;  // step count (not a time slot)
     }
     if (a.prof && tid == 0 && (a.prof_t0 < 0 || t == a.prof_t0))
-        for (int i = 0; i < 16; ++i) atomicAdd((unsigned long long*)&a.prof[i], (unsigned long long)pt[i]);
+        for (int i = 0; i < 24; ++i) atomicAdd((unsigned long long*)&a.prof[i], (unsigned long long)pt[i]);
 #undef K1_TICK
+#undef K1_SUB
 }

@@ -260,12 +260,13 @@ struct Plan {
     bool far_side = false;   // one GPU: far H/T tiles' right updates on the side stream (HT_FAR_SIDE)
     int wy = 0, QP = 0;      // WY window blocks (chain.cuh ChainParams::wy; accum_wy_kernel)
     int hlag = 1;          // helper row split (ChaseArgs::hlag): 0 for r >= 32 (HT_HELPER_LAG overrides)
+    int rqu = 0;           // K1 opposite reflector by RQ update (rqu.cuh; HT_RQU=0 disables)
     size_t mrg_bytes = 0;
     const unsigned long long* gate = nullptr;  // device verdict words of the input check (nullptr: none)
     bool is_root() const { return comm == nullptr || rank == root; }
     bool qz() const { return Q || Z; }
     bool same(const Plan& o) const {
-        return n == o.n && r == o.r && q == o.q && strip_cap == o.strip_cap && helpers == o.helpers && P == o.P && qz_late == o.qz_late && qz_groups == o.qz_groups && far_side == o.far_side && wy == o.wy && hlag == o.hlag && G == o.G && emul_ht == o.emul_ht && gate == o.gate && H == o.H && ldh == o.ldh &&
+        return n == o.n && r == o.r && q == o.q && strip_cap == o.strip_cap && helpers == o.helpers && P == o.P && qz_late == o.qz_late && qz_groups == o.qz_groups && far_side == o.far_side && wy == o.wy && hlag == o.hlag && rqu == o.rqu && G == o.G && emul_ht == o.emul_ht && gate == o.gate && H == o.H && ldh == o.ldh &&
                T == o.T && ldt == o.ldt && Q == o.Q && ldq == o.ldq && Z == o.Z && ldz == o.ldz;
     }
 };
@@ -281,12 +282,15 @@ inline int64_t mcatch_st(int q, int r) { return (int64_t)(q + r - 1) * mcatch_ld
 template <typename S>
 struct Workspace {
     S *U[NUV] = {}, *V[NUV] = {}, *MU[NUV] = {}, *MV[NUV] = {}, *Zr = nullptr, *Qr = nullptr, *Tr = nullptr, *Mg = nullptr;
+    double* Fg = nullptr;  // RQ-update hand-over (Kmax x 2 x 64 x 64), kept across groups
+    double* Fb = nullptr;  // rqu 2: caught-up column b per window (Kmax x 64)
+    int* Fdone = nullptr;  // rqu 2: hand-over generation per window (Kmax)
     unsigned long long* lag = nullptr;  // HT_LAG_CHECK stamps (one group)
     S* xfer = nullptr;                  // far H/T tile transfers (2 CH_BM n scalars)
     S* emu[16] = {};                    // emulated ranks' H/T copies
     int* prog = nullptr;
     long long* k1prof = nullptr;
-    long long k1prof_host[32] = {0};  // [0,16) K1, [16,24) right chains, [24,32) left chains
+    long long k1prof_host[40] = {0};  // [0,16) K1, [16,24) K1 sub-phases, [24,32) right chains, [32,40) left chains
     cudaStream_t side = nullptr;
     cudaEvent_t ev_uv[NUV] = {}, ev_qz[NUV] = {}, ev_k2[NUV] = {};
     bool async = true;
@@ -312,13 +316,18 @@ struct Workspace {
         CK(mal((void**)&Qr, rec));
         CK(mal((void**)&Tr, tf));
         if (chase_dense_catchup<S>(p.r)) CK(mal((void**)&Mg, (size_t)p.Kmax * mcatch_st(p.q, p.r) * sizeof(S)));
+        if (p.rqu) CK(mal((void**)&Fg, (size_t)p.Kmax * 2 * 64 * 64 * sizeof(double)));
+        if (p.rqu == 2) {
+            CK(mal((void**)&Fb, (size_t)p.Kmax * 64 * sizeof(double)));
+            CK(mal((void**)&Fdone, (size_t)p.Kmax * sizeof(int)));
+        }
         CK(mal((void**)&prog, (size_t)(5 * p.q + 2) * sizeof(int)));
         if (p.shard_ht() && !p.emul_ht) CK(mal((void**)&xfer, (size_t)2 * CH_BM * p.n * sizeof(S)));
         if (getenv("HT_LAG_CHECK") && async)
             CK(mal((void**)&lag, (size_t)2 * p.q * p.Kmax * 4 * sizeof(unsigned long long)));
         if (k1p) {
-            CK(mal((void**)&k1prof, 32 * sizeof(long long)));
-            CK(cudaMemsetAsync(k1prof, 0, 32 * sizeof(long long), stream));
+            CK(mal((void**)&k1prof, 40 * sizeof(long long)));
+            CK(cudaMemsetAsync(k1prof, 0, 40 * sizeof(long long), stream));
         }
         if (p.qz()) {
             int lo = 0, hi = 0;
@@ -352,6 +361,12 @@ struct Workspace {
         CK(fr(Tr));
         if (Mg) CK(fr(Mg));
         Mg = nullptr;
+        if (Fg) CK(fr(Fg));
+        Fg = nullptr;
+        if (Fb) CK(fr(Fb));
+        Fb = nullptr;
+        if (Fdone) CK(fr(Fdone));
+        Fdone = nullptr;
         CK(fr(prog));
         CK(fr(k1prof));
         CK(fr(lag));
@@ -385,8 +400,18 @@ void print_k1prof(const long long* h) {
     for (int i = 0; i < 16; ++i)
         if (i != 11 && h[i]) fprintf(stderr, " %s=%.0f", nm[i], h[i] / steps);
     fprintf(stderr, " all=%.0f\n", tot / steps);
+    // sub-phases (parts of the slots above): the RQ update (rqu.cuh)
+    const char* sn[8] = {"rqu_loadwait", "rqu_A", "rqu_BC|solve", "rqu_D|Qx", "rqu_handoff", "rqu_Dchain", "S4_QB_tid0", "S4_T_tidNT/2"};
+    bool any = false;
+    for (int i = 16; i < 24; ++i) any |= h[i] != 0;
+    if (any) {
+        fprintf(stderr, "K1 sub-phase cycles per step:");
+        for (int i = 16; i < 24; ++i)
+            if (h[i]) fprintf(stderr, " %s=%.0f", sn[i - 16], h[i] / steps);
+        fprintf(stderr, "\n");
+    }
     for (int c = 0; c < 2; ++c) {  // apply chains: the longest tile (tile 0 of H)
-        const long long* g = h + 16 + 8 * c;
+        const long long* g = h + 24 + 8 * c;
         const double st = g[5] > 0 ? (double)g[5] : 1.0;
         fprintf(stderr, "%s chain, profiled tile of H (HT_CHAIN_PROF_TILE), cycles per step: wait+prefetch=%.0f mma=%.0f epilogue=%.0f "
                         "staircase=%.0f store=%.0f (steps %lld, merged %lld, with staircase %lld)\n",
@@ -508,6 +533,7 @@ int enqueue_groups(const Plan<S>& p, Workspace<S>& ws, cudaStream_t stream, bool
             CK(cudaEventCreate(&e));
             ev.push_back(e);
         }
+    if (ws.Fdone) CK(cudaMemsetAsync(ws.Fdone, 0, (size_t)p.Kmax * sizeof(int), stream));
     if (qz) {
         CK(cudaEventRecord(ws.ev_qz[0], stream));  // workspace allocations visible to the side stream
         CK(cudaStreamWaitEvent(ws.side, ws.ev_qz[0], 0));
@@ -536,6 +562,11 @@ int enqueue_groups(const Plan<S>& p, Workspace<S>& ws, cudaStream_t stream, bool
                             mcatch_ld(q, r), mcatch_st(q, r), ws.prog, p.strip_cap,
                             p.helpers, ws.k1prof, getenv("HT_K1PROF_T") ? atoi(getenv("HT_K1PROF_T")) : -1,
                             p.hlag, p.gate, ws.lag};
+            ca.Fg = ws.Fg;
+            ca.fst = (int64_t)2 * 64 * 64;
+            ca.rqu = p.rqu;
+            ca.Fb = ws.Fb;
+            ca.Fdone = ws.Fdone;
             const size_t lag_elems = (size_t)2 * qp * K * (1 + p.helpers);
             if (ws.lag) CK(cudaMemsetAsync(ws.lag, 0, lag_elems * sizeof(unsigned long long), stream));
             void* kargs[] = {&ca};
@@ -619,7 +650,7 @@ int enqueue_groups(const Plan<S>& p, Workspace<S>& ws, cudaStream_t stream, bool
         if (root) {
             ChainParams<S> pr{n, r, qp, j1, K, {{p.H, p.ldh, ws.V[bsel], ws.MV[bsel], CM_AB_RIGHT, 0, tiles - nf, nf},
                                                 {p.T, p.ldt, ws.V[bsel], ws.MV[bsel], CM_AB_RIGHT, 0, tiles - nf, nf}}, 2, ws.Zr, p.P,
-                              chain_spread(p.nsm), ws.k1prof ? ws.k1prof + 16 : nullptr,
+                              chain_spread(p.nsm), ws.k1prof ? ws.k1prof + 24 : nullptr,
                               getenv("HT_CHAIN_PROF_TILE") ? atoi(getenv("HT_CHAIN_PROF_TILE")) : 0,
                               !(getenv("HT_STAIR_FIRST") && atoi(getenv("HT_STAIR_FIRST")) == 0)};
             pr.gate = p.gate;
@@ -628,7 +659,7 @@ int enqueue_groups(const Plan<S>& p, Workspace<S>& ws, cudaStream_t stream, bool
             if (int rc = chain<S>(pr, WP, 2 * (tiles - nf), r, q, stream)) return rc;
             ChainParams<S> pl{n, r, qp, j1, K, {{p.H, p.ldh, ws.U[bsel], ws.MU[bsel], CM_A_LEFT, 1, tiles, 0},
                                                 {p.T, p.ldt, ws.U[bsel], ws.MU[bsel], CM_B_LEFT, 1, tiles, 0}}, 2, ws.Zr, p.P,
-                              chain_spread(p.nsm), ws.k1prof ? ws.k1prof + 24 : nullptr,
+                              chain_spread(p.nsm), ws.k1prof ? ws.k1prof + 32 : nullptr,
                               getenv("HT_CHAIN_PROF_TILE") ? atoi(getenv("HT_CHAIN_PROF_TILE")) : 0};
             pl.gate = p.gate;
             pl.wy = p.wy;
@@ -920,11 +951,13 @@ int run(int64_t n64, int64_t r64, S* H, int64_t ldh, S* T, int64_t ldt, S* Q, in
     const int Kmax = 1 + (n - 1 - 2) / r;
     // shared memory of a chase CTA; what the fixed buffers leave goes to staged strip rows
     // (HT_CHASE_SMEM_KB overrides; 224 KB measured no faster than 200 at r = 32, 64)
-    const int chase_budget = (getenv("HT_CHASE_SMEM_KB") ? atoi(getenv("HT_CHASE_SMEM_KB")) : 200) * 1024;
-    const size_t chase_base = chase_smem_elems<S>(r, q, 0) * sizeof(S);
+    // K1's opposite reflector by RQ update (rqu.cuh, real 32 < r <= 64; HT_RQU=0: Householder RQ per step)
+    const int rqu = rqu_supported_r<S>(r) && !(getenv("HT_RQU") && atoi(getenv("HT_RQU")) == 0);
+    const int chase_budget = (getenv("HT_CHASE_SMEM_KB") ? atoi(getenv("HT_CHASE_SMEM_KB")) : (rqu ? 224 : 200)) * 1024;
+    const size_t chase_base = chase_smem_elems<S>(r, q, 0, rqu) * sizeof(S);
     const int strip_cap = (int)std::max<int64_t>(0, ((int64_t)chase_budget - (int64_t)chase_base) /
                                                         (int64_t)((r + 1) * sizeof(S)));
-    const size_t chase_bytes = chase_smem_elems<S>(r, q, strip_cap) * sizeof(S);
+    const size_t chase_bytes = chase_smem_elems<S>(r, q, strip_cap, rqu) * sizeof(S);
     const bool acc_pre = accum_smem_bytes<S>(r, q, true) <= 200 * 1024;
     const size_t acc_bytes = accum_smem_bytes<S>(r, q, acc_pre);
     const void* chase_fn = chase_kernel_for<S>(r);
@@ -964,6 +997,8 @@ int run(int64_t n64, int64_t r64, S* H, int64_t ldh, S* T, int64_t ldt, S* Q, in
     Plan<S> pl{n, r, q, WP, LDB, Kmax, strip_cap, chase_bytes, acc_bytes, chase_fn, H, ldh, T, ldt, Q, ldq, Z, ldz,
                std::max(8, nsm - (1 + helpers) * q)};
     pl.helpers = helpers;
+    // rqu 2 (default with helpers): the sweep solves for the direction, a helper runs the RQ update
+    pl.rqu = rqu ? ((helpers > 0 && !(getenv("HT_RQU") && atoi(getenv("HT_RQU")) == 1)) ? 2 : 1) : 0;
     pl.wy = wy;
     pl.QP = QPw;
     pl.P = PM;
