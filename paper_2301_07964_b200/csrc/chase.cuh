@@ -60,6 +60,9 @@ struct ChaseArgs {
                         // triangular solve, the RQ update (hand-over) by the sweep's helper h = k mod H
     double* Fb = nullptr;  // rqu 2: the caught-up column b of step (j,k) per k (MAXM each)
     int* Fdone = nullptr;  // rqu 2: per k, j+1 once the hand-over of sweep j's step k is in Fg
+    int* Freq = nullptr;   // rqu 2, MAXM 128: per k, j+1 when sweep j's solve failed (direction requested)
+    int* Fdirok = nullptr; // ... j+1 once the helper put Q~(1,:) in Fdir
+    double* Fdir = nullptr;
 };
 
 // shared-memory buffers of the RQ update (chase_kernel carves them; helpers use them too)
@@ -572,9 +575,9 @@ __host__ __device__ constexpr bool chase_dense_catchup(int r) {
 
 // K1's RQ-update path (rqu.cuh): real fp64, 32 < r <= 64 (MAXM = 64)
 template <typename S, int MAXM>
-__host__ __device__ constexpr bool rqu_supported() { return sizeof(S) == 8 && MAXM == 64; }
+__host__ __device__ constexpr bool rqu_supported() { return sizeof(S) == 8 && (MAXM == 64 || MAXM == 128); }
 template <typename S>
-__host__ __device__ inline bool rqu_supported_r(int r) { return sizeof(S) == 8 && r > 32 && r <= 64; }
+__host__ __device__ inline bool rqu_supported_r(int r) { return sizeof(S) == 8 && r > 32 && r <= 128; }
 constexpr int CHASE_NT_RQU = 256;
 
 template <typename S>
@@ -592,7 +595,7 @@ __host__ __device__ inline size_t chase_smem_elems(int r, int qp, int strip_cap,
            5 * (size_t)(qp + 8) +        // WY temporaries
            (overlay ? 0 : XL + (size_t)r * (r + 1) + (size_t)qp * (r + 1) + (size_t)qp * (qp + 1)) +  // prefetch set
            (chase_dense_catchup<S>(r) ? 2 * (size_t)w * (w | 1) + 2 * (size_t)(w + 1) : 0) +  // M_t, M_t(k+1), tmp
-           (rqu ? RQUCfg<CHASE_NT_RQU, 64>::extra : 0) +  // RQ update: Q0, w parts, rotations
+           (rqu ? (r <= 64 ? RQUCfg<CHASE_NT_RQU, 64>::extra : RQUCfg<CHASE_NT_RQU, 128>::extra) : 0) +  // RQ update
            (size_t)strip_cap * (r + 1);  // staged strip rows
 }
 
@@ -608,7 +611,7 @@ __host__ __device__ inline size_t chase_smem_elems(int r, int qp, int strip_cap,
 // helper j's items <= k -- so with lag 0 the y column is loaded at the step start instead of
 // being prefetched during step k-2 (the B block's last column is patched from the caught-up y
 // anyway); sweep j itself never reads those rows again.
-template <typename S, int NT, int MAXM>
+template <typename S, int NT, int MAXM, bool RQK>
 __device__ __forceinline__ void far_strip_helper(const ChaseArgs<S>& a, int t, int h, S* sm, const RQUBufs& rb) {
     const int H = a.helpers;
     constexpr int RB = 64;  // row block: helper h owns blocks h, h+H, ... (relative to j1)
@@ -623,7 +626,95 @@ __device__ __forceinline__ void far_strip_helper(const ChaseArgs<S>& a, int t, i
     constexpr int CPR = MAXM / SPR;
     const int part = tid % SPR, c0 = part * CPR;
     long long hw = 0, hx = 0, tc = clock64();  // profile: cycles waiting / working (helper 0)
+    // rqu 2 (rqu.cuh): the RQ update of step (j,k) and its hand-over to sweep j+1 (helper k mod H).
+    // MAXM 64: R0 and Q0 in their own buffers, Q rotated concurrently with the chain.  MAXM 128: R0
+    // in the B block's buffer, R~ handed over first, then Q0 rotated in the same buffer; a sweep whose
+    // solve failed requests the direction Q~(1,:) early (Freq) and waits for it (Fdirok).
+    constexpr bool RQH = RQK && rqu_supported<S, MAXM>();
+    constexpr bool RQU64 = RQH && MAXM == 64, RQU128 = RQH && MAXM == 128;
+    __shared__ int hreq;
+    int early_k = -1;  // step whose Q~ is already in shared memory (early request)
+    auto fwork = [&](int k, int stage) {  // stage 0: all; 1: up to Q~ (early); 2: hand-over of W only
+        if constexpr (RQH) {
+            constexpr int RLD = RQUCfg<NT, MAXM>::RLD;
+            const int i1 = j + k * r + 1, m = min(j + (k + 1) * r, n) - i1 + 1;
+            const bool hasB = i1 + r - 1 <= n;
+            const int f = hasB ? m - 1 : m;
+            double* FR = a.Fg + (int64_t)k * a.fst;
+            double* FW = FR + MAXM * MAXM;
+            const double* qrec = reinterpret_cast<const double*>(a.Qr + ((int64_t)t * K + k) * (r + 1));
+            const double* zrec = reinterpret_cast<const double*>(a.Zr + ((int64_t)t * K + k) * (r + 1));
+            if (stage != 2) {
+                if constexpr (RQU64) rqu_load_block<NT, MAXM>(rb.Qs, FW, f, false);
+                rqu_load_block<NT, MAXM>(rb.Rs, FR, f, true);
+                if (hasB)
+                    for (int i = tid; i < m; i += NT) {
+                        rb.Rs[i * RLD + (m - 1)] = ldcg(a.Fb + (int64_t)k * MAXM + i);
+                        if constexpr (RQU64) {
+                            rb.Qs[(m - 1) * RLD + i] = (i == m - 1) ? 1.0 : 0.0;
+                            rb.Qs[i * RLD + (m - 1)] = (i == m - 1) ? 1.0 : 0.0;
+                        }
+                    }
+                for (int c = tid; c < m; c += NT) rb.v[c] = ldcg(qrec + c);
+                const double tau = ldcg(qrec + r);
+                __syncthreads();
+                rqu_direction<NT, MAXM>(m, rb.v, tau, rb.Rs, rb.Qs, rb.wpart, rb.cs1, rb.cs2, rb.uu);
+                if constexpr (RQU128) {  // R~ out, then Q0 into the same buffer
+                    rqu_handoff_R<NT, MAXM>(m, rb.Rs, FR);
+                    __syncthreads();
+                    rqu_load_block<NT, MAXM>(rb.Rs, FW, f, false);
+                    if (hasB)
+                        for (int i = tid; i < m; i += NT) {
+                            rb.Rs[(m - 1) * RLD + i] = (i == m - 1) ? 1.0 : 0.0;
+                            rb.Rs[i * RLD + (m - 1)] = (i == m - 1) ? 1.0 : 0.0;
+                        }
+                    __syncthreads();
+                    rqu_q_apply<NT, MAXM>(m, rb.Rs, rb.cs1, rb.cs2, rb.uu);
+                    for (int i = tid; i < MAXM; i += NT) rb.cs2[2 * i] = RQU_SENTINEL;
+                    if (stage == 1) {  // the direction for the waiting sweep
+                        for (int c = tid; c < m; c += NT) a.Fdir[(int64_t)k * MAXM + c] = rb.uu[c];
+                        __syncthreads();
+                        if (tid == 0) {
+                            __threadfence();
+                            st_release(&a.Fdirok[k], j + 1);
+                        }
+                        return;
+                    }
+                }
+            }
+            for (int c = tid; c < m; c += NT) rb.z[c] = ldcg(zrec + c);
+            const double sig = ldcg(zrec + r);
+            __syncthreads();
+            if constexpr (RQU64) rqu_handoff<NT, MAXM>(m, rb.Rs, rb.Qs, rb.z, sig, FR, FW);
+            else rqu_handoff_W<NT, MAXM>(m, rb.Rs, rb.z, sig, FW);
+            __syncthreads();
+            if (tid == 0) {
+                __threadfence();
+                st_release(&a.Fdone[k], j + 1);
+            }
+        }
+    };
     for (int k = 0; k < kcount; ++k) {
+        if constexpr (RQU128) {
+            // the designated helper also answers an early request of the sweep (its solve failed)
+            if (a.rqu == 2 && k % H == h) {
+                if (tid == 0) {
+                    int req = 0;
+                    while (ld_relaxed(&a.prog[t]) < k + 1)
+                        if (ld_relaxed(&a.Freq[k]) >= j + 1) {
+                            req = 1;
+                            break;
+                        }
+                    asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
+                    hreq = req;
+                }
+                __syncthreads();
+                if (hreq) {
+                    fwork(k, 1);
+                    early_k = k;
+                }
+            }
+        }
         if (tid == 0) {
             if (ld_acquire(&a.prog[t]) < k + 1)
                 while (ld_relaxed(&a.prog[t]) < k + 1) {
@@ -705,43 +796,11 @@ __device__ __forceinline__ void far_strip_helper(const ChaseArgs<S>& a, int t, i
             if (a.trace) a.trace[((int64_t)qp * K + ((int64_t)t * H + h) * K + k) * 2 + 1] = gtimer();
             st_release(&hprog[t * H + h], k + 1);
         }
-        if constexpr (rqu_supported<S, MAXM>()) {
-            // rqu 2: the RQ update of step (j,k) and its hand-over to sweep j+1 (rqu.cuh), unless the
-            // sweep fell back to doing it itself; sweep j+1 waits for Fdone[k] = j+1 at its step k
+        if constexpr (RQH) {
+            // rqu 2: the RQ update of step (j,k) and its hand-over (unless the sweep did it: MAXM 64)
             const int jb = j + max(0, (k - 1) * r + 1);
-            if (a.rqu == 2 && k % H == h && m >= 2 && jb <= n && ld_acquire(&a.Fdone[k]) < j + 1) {
-                constexpr int RLD = RQUCfg<NT, MAXM>::RLD;
-                const bool hasB = i1 + r - 1 <= n;
-                const int f = hasB ? m - 1 : m;
-                double* FR = a.Fg + (int64_t)k * a.fst;
-                double* FW = FR + MAXM * MAXM;
-                for (int e = tid; e < f * f; e += NT) {
-                    const int p = e / f, c = e - p * f;
-                    rb.Qs[p * RLD + c] = ldcg(FW + p * MAXM + c);
-                    if (c >= p) rb.Rs[p * RLD + c] = ldcg(FR + p * MAXM + c);
-                }
-                if (hasB)
-                    for (int i = tid; i < m; i += NT) {
-                        rb.Rs[i * RLD + (m - 1)] = ldcg(a.Fb + (int64_t)k * MAXM + i);
-                        rb.Qs[(m - 1) * RLD + i] = (i == m - 1) ? 1.0 : 0.0;
-                        rb.Qs[i * RLD + (m - 1)] = (i == m - 1) ? 1.0 : 0.0;
-                    }
-                const double* qrec = reinterpret_cast<const double*>(a.Qr + ((int64_t)t * K + k) * (r + 1));
-                const double* zrec = reinterpret_cast<const double*>(a.Zr + ((int64_t)t * K + k) * (r + 1));
-                for (int c = tid; c < m; c += NT) {
-                    rb.v[c] = ldcg(qrec + c);
-                    rb.z[c] = ldcg(zrec + c);
-                }
-                const double tau = ldcg(qrec + r), sig = ldcg(zrec + r);
-                __syncthreads();
-                rqu_direction<NT, MAXM>(m, rb.v, tau, rb.Rs, rb.Qs, rb.wpart, rb.cs1, rb.cs2, rb.uu);
-                rqu_handoff<NT, MAXM>(m, rb.Rs, rb.Qs, rb.z, sig, FR, FW);
-                __syncthreads();
-                if (tid == 0) {
-                    __threadfence();
-                    st_release(&a.Fdone[k], j + 1);
-                }
-            }
+            if (a.rqu == 2 && k % H == h && m >= 2 && jb <= n && (RQU128 || ld_acquire(&a.Fdone[k]) < j + 1))
+                fwork(k, early_k == k ? 2 : 0);
         }
         if (a.prof && tid == 0) {
             const long long now = clock64();
@@ -755,7 +814,9 @@ __device__ __forceinline__ void far_strip_helper(const ChaseArgs<S>& a, int t, i
     }
 }
 
-template <typename S, int NT, int MAXM>
+// RQK: the RQ-update instantiation (rqu.cuh; launched with a.rqu != 0) -- a separate kernel, so that
+// neither path's register allocation carries the other's (the warp-row RQ of r > 64 needs 255)
+template <typename S, int NT, int MAXM, bool RQK = false>
 __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
     if (input_rejected(a.gate)) return;
     extern __shared__ __align__(16) unsigned char smraw[];
@@ -805,20 +866,24 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
     S* Msm1 = MK ? Msm0 + (size_t)w * MLD : Msm0;
     S* mtmp = MK ? Msm1 + (size_t)w * MLD : Msm0;  // 2 (w+1): catch-up outputs / M update row
     S* strip0 = MK ? mtmp + 2 * (size_t)(w + 1) : Msm0;
-    // RQ update (rqu.cuh): R0 overlays the RQ ring, Q0 / w parts / rotations before the strip
-    constexpr bool RQU_OK = rqu_supported<S, MAXM>();
+    // RQ update (rqu.cuh): R0 overlays the RQ ring (MAXM 64) or the B block (MAXM 128, after its
+    // write-back); Q0 (MAXM 64) / w parts / rotations / x / b before the strip
+    constexpr bool RQU_OK = RQK && rqu_supported<S, MAXM>();
+    constexpr bool RQU64 = RQU_OK && MAXM == 64, RQU128 = RQU_OK && MAXM == 128;
     const bool rqu = RQU_OK && a.rqu != 0;
-    using RQC = RQUCfg<NT, (RQU_OK ? MAXM : 64)>;
+    constexpr int RQM = RQU_OK ? MAXM : 64;
+    using RQC = RQUCfg<NT, RQM>;
     constexpr int RLD = RQC::RLD;
-    double* const Rs = reinterpret_cast<double*>(ring);
-    double* const Qs = reinterpret_cast<double*>(strip0);
-    double* const wpart = Qs + (size_t)RQC::RLD * (RQU_OK ? MAXM : 64);
-    double* const cs1 = wpart + (size_t)RQC::NPART * (RQU_OK ? MAXM : 64);
-    double* const cs2 = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(cs1 + 2 * (RQU_OK ? MAXM : 64)) + 15) & ~(uintptr_t)15);
-    double* const xs = cs2 + 2 * (RQU_OK ? MAXM : 64);
+    double* const Rs = reinterpret_cast<double*>(RQU128 ? Cb0 : ring);
+    double* const Qs = RQC::QCONC ? reinterpret_cast<double*>(strip0) : Rs;
+    double* const wpart = reinterpret_cast<double*>(strip0) + (RQC::QCONC ? (size_t)RLD * RQM : 0);
+    double* const cs1 = wpart + (size_t)RQC::NPART * RQM;
+    double* const cs2 = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(cs1 + 2 * RQM) + 15) & ~(uintptr_t)15);
+    double* const xs = cs2 + 2 * RQM;
+    double* const bcol = xs + RQM;
     __shared__ int rqu_ok;
     if (rqu)
-        for (int i = threadIdx.x; i < (RQU_OK ? MAXM : 64); i += NT) cs2[2 * i] = RQU_SENTINEL;
+        for (int i = threadIdx.x; i < RQM; i += NT) cs2[2 * i] = RQU_SENTINEL;
     S* strip = rqu ? strip0 + RQC::extra : strip0;  // strip_cap rows x (r+1) (row-major)
     const int LDC = r + 1;
     // sweep index by ticket (not blockIdx): a CTA only ever waits on a sweep whose CTA already
@@ -830,7 +895,7 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
     const int t = t_sh / (1 + a.helpers);
     if (t >= qp) return;
     if (role > 0) {
-        far_strip_helper<S, NT, MAXM>(a, t, role - 1, sm,
+        far_strip_helper<S, NT, MAXM, RQK>(a, t, role - 1, sm,
                                       RQUBufs{Rs, Qs, wpart, cs1, cs2, xs, reinterpret_cast<double*>(vq),
                                               reinterpret_cast<double*>(vz), reinterpret_cast<double*>(uu)});
         return;
@@ -985,7 +1050,7 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
         K1_TICK(1);
         if constexpr (RQU_OK) {
             if (rqu) {  // sweep j-1's hand-over for window k (rqu.cuh), waited for before the RQ update
-                if (gen && j > 1) {
+                if (RQU64 && gen && j > 1) {
                     const int f = hasB ? m - 1 : m;
                     const double* FR = a.Fg + (int64_t)k * a.fst;
                     const double* FW = FR + MAXM * MAXM;
@@ -1174,12 +1239,13 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
                     if constexpr (RQU_OK) {
                         if (rqu) {  // R0 / Q0 from B0 (still unreduced in Cb): see rqu.cuh
                             if (j == 1) {  // T itself: R0 = B0 (upper triangular), Q0 = I
-                                for (int e = tid; e < m * m; e += NT) {
-                                    const int p = e / m, c = e - p * m;
-                                    Qs[p * RLD + c] = (p == c) ? 1.0 : 0.0;
-                                    if (c >= p) Rs[p * RLD + c] = re(Cb[p + c * LDC]);
-                                }
-                                if (a.rqu == 2) {  // the helper reads the hand-over form of it
+                                if constexpr (RQU64)
+                                    for (int e = tid; e < m * m; e += NT) {
+                                        const int p = e / m, c = e - p * m;
+                                        Qs[p * RLD + c] = (p == c) ? 1.0 : 0.0;
+                                        if (c >= p) Rs[p * RLD + c] = re(Cb[p + c * LDC]);
+                                    }
+                                if (a.rqu == 2) {  // the helper (and MAXM 128's sweep) read the hand-over form
                                     const int f = hasB ? m - 1 : m;
                                     double* FR = a.Fg + (int64_t)k * a.fst;
                                     for (int e = tid; e < f * f; e += NT) {
@@ -1188,15 +1254,19 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
                                         if (c >= p) FR[p * MAXM + c] = re(Cb[p + c * LDC]);
                                     }
                                 }
-                            } else if (hasB) {  // last column b = B0(:, m), Q0 = diag(W, 1)
+                            } else if (RQU64 && hasB) {  // last column b = B0(:, m), Q0 = diag(W, 1)
                                 for (int i = tid; i < m; i += NT) {
                                     Rs[i * RLD + (m - 1)] = re(Cb[i + (m - 1) * LDC]);
                                     Qs[(m - 1) * RLD + i] = (i == m - 1) ? 1.0 : 0.0;
                                     Qs[i * RLD + (m - 1)] = (i == m - 1) ? 1.0 : 0.0;
                                 }
                             }
-                            if (a.rqu == 2 && hasB)  // b for the helper's RQ update
-                                for (int i = tid; i < m; i += NT) a.Fb[(int64_t)k * MAXM + i] = re(Cb[i + (m - 1) * LDC]);
+                            if (a.rqu == 2 && hasB)  // b for the helper's RQ update (and MAXM 128's R0)
+                                for (int i = tid; i < m; i += NT) {
+                                    const double b = re(Cb[i + (m - 1) * LDC]);
+                                    a.Fb[(int64_t)k * MAXM + i] = b;
+                                    if (RQU128) bcol[i] = b;
+                                }
                         }
                     }
                 }
@@ -1300,6 +1370,15 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
                     for (int cc = warp; cc < m; cc += NW)
                         for (int ii = lane; ii < m; ii += 32) IDX(a.B, a.ldb, i1 + ii, i1 + cc) = Cb[ii + cc * LDC];
                     __syncthreads();
+                    if constexpr (RQU128) {
+                        if (rqu) {  // R0 into the block's buffer: sweep j-1's hand-over (L2 reads) and b
+                            const int f = hasB ? m - 1 : m;
+                            rqu_load_block<NT, MAXM>(Rs, a.Fg + (int64_t)k * a.fst, f, true);
+                            if (hasB)
+                                for (int i = tid; i < m; i += NT) Rs[i * RLD + (m - 1)] = bcol[i];
+                            __syncthreads();
+                        }
+                    }
                 }
                 K1_TICK(3);
                 // ---- (S5) RQ of the block -> Z_k^j ---------------------------------------------
@@ -1314,7 +1393,7 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
                     else k1_wait_group<0>();
                     __syncthreads();
                     K1_SUB(16, 6);
-                    if constexpr (RQU_OK) {
+                    if constexpr (RQU64) {
                         const double* vd = reinterpret_cast<const double*>(vq);
                         double* ud = reinterpret_cast<double*>(uu);
                         if (a.rqu == 2)
@@ -1322,8 +1401,25 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
                                                                 a.prof ? pt : nullptr, &tc);
                         if (a.rqu != 2 || rqu_fallback)
                             rqu_direction<NT, MAXM>(m, vd, re(tau), Rs, Qs, wpart, cs1, cs2, ud, a.prof ? pt : nullptr, &tc);
+                    } else if constexpr (RQU128) {  // Q0 read from the hand-over in L2
+                        const double* vd = reinterpret_cast<const double*>(vq);
+                        double* ud = reinterpret_cast<double*>(uu);
+                        const double* FW = a.Fg + (int64_t)k * a.fst + MAXM * MAXM;
+                        if (!rqu_solve<NT, MAXM>(m, vd, re(tau), Rs, Qs, wpart, xs, ud, &rqu_ok, a.prof ? pt : nullptr, &tc,
+                                                 FW, hasB)) {
+                            // the designated helper runs the RQ update now and returns Q~(1,:)
+                            if (tid == 0) {
+                                __threadfence();
+                                st_release(&a.Freq[k], j + 1);
+                                while (ld_relaxed(&a.Fdirok[k]) < j + 1) {
+                                }
+                                asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
+                            }
+                            __syncthreads();
+                            for (int c = tid; c < m; c += NT) ud[c] = ldcg(a.Fdir + (int64_t)k * MAXM + c);
+                        }
                     }
-                } else {
+                } else if constexpr (!RQU_OK) {
                 if (PF && k + 1 < kcount) {  // next step's inputs land while the RQ runs (issued by
                     // the warps the RQ does not use, if any)
                     constexpr int RQT = rq_nthr<S, MAXM>();
@@ -1478,7 +1574,7 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
                 S* zr = a.Zr + ((int64_t)t * K + k) * (r + 1);
                 for (int c = tid; c < m; c += NT) zr[c] = vz[c];
                 if (tid == 0) zr[r] = sig;
-                if constexpr (RQU_OK)
+                if constexpr (RQU64)
                     if (rqu && (a.rqu == 1 || rqu_fallback)) {  // hand-over to sweep j+1 (read at its step k)
                         K1_TICK(5);
                         double* FR = a.Fg + (int64_t)k * a.fst;

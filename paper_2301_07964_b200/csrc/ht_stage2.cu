@@ -179,13 +179,14 @@ size_t chain_bytes_rt(int WP, int r, int q, int P = 1, int QP = 0) {
 
 // K1 instantiation for the reflector length (the RQ keeps [C; P] rows in registers)
 template <typename S>
-const void* chase_kernel_for(int r) {
+const void* chase_kernel_for(int r, bool rqu) {
     if (r <= 8) return (const void*)chase_kernel<S, CHASE_NT, 8>;
     if (r <= 16) return (const void*)chase_kernel<S, CHASE_NT, 16>;
     if (r <= 32) return (const void*)chase_kernel<S, CHASE_NT, 32>;
     if constexpr (sizeof(S) == 8) {  // complex: r <= 32 (registers of the complex RQ)
-        if (r <= 64) return (const void*)chase_kernel<S, CHASE_NT, 64>;
-        if (r <= 128) return (const void*)chase_kernel<S, CHASE_NT, 128>;
+        if (r <= 64) return rqu ? (const void*)chase_kernel<S, CHASE_NT, 64, true> : (const void*)chase_kernel<S, CHASE_NT, 64>;
+        if (r <= 128)
+            return rqu ? (const void*)chase_kernel<S, CHASE_NT, 128, true> : (const void*)chase_kernel<S, CHASE_NT, 128>;
     }
     return nullptr;
 }
@@ -283,8 +284,11 @@ template <typename S>
 struct Workspace {
     S *U[NUV] = {}, *V[NUV] = {}, *MU[NUV] = {}, *MV[NUV] = {}, *Zr = nullptr, *Qr = nullptr, *Tr = nullptr, *Mg = nullptr;
     double* Fg = nullptr;  // RQ-update hand-over (Kmax x 2 x 64 x 64), kept across groups
-    double* Fb = nullptr;  // rqu 2: caught-up column b per window (Kmax x 64)
+    double* Fb = nullptr;  // rqu 2: caught-up column b per window (Kmax x MAXM)
     int* Fdone = nullptr;  // rqu 2: hand-over generation per window (Kmax)
+    int* Freq = nullptr;   // rqu 2, MAXM 128: early direction requests / answers per window
+    int* Fdirok = nullptr;
+    double* Fdir = nullptr;
     unsigned long long* lag = nullptr;  // HT_LAG_CHECK stamps (one group)
     S* xfer = nullptr;                  // far H/T tile transfers (2 CH_BM n scalars)
     S* emu[16] = {};                    // emulated ranks' H/T copies
@@ -316,10 +320,14 @@ struct Workspace {
         CK(mal((void**)&Qr, rec));
         CK(mal((void**)&Tr, tf));
         if (chase_dense_catchup<S>(p.r)) CK(mal((void**)&Mg, (size_t)p.Kmax * mcatch_st(p.q, p.r) * sizeof(S)));
-        if (p.rqu) CK(mal((void**)&Fg, (size_t)p.Kmax * 2 * 64 * 64 * sizeof(double)));
+        const size_t rm = p.r <= 64 ? 64 : 128;  // MAXM of the RQ update
+        if (p.rqu) CK(mal((void**)&Fg, (size_t)p.Kmax * 2 * rm * rm * sizeof(double)));
         if (p.rqu == 2) {
-            CK(mal((void**)&Fb, (size_t)p.Kmax * 64 * sizeof(double)));
-            CK(mal((void**)&Fdone, (size_t)p.Kmax * sizeof(int)));
+            CK(mal((void**)&Fb, (size_t)p.Kmax * rm * sizeof(double)));
+            CK(mal((void**)&Fdone, (size_t)3 * p.Kmax * sizeof(int)));  // Fdone, Freq, Fdirok
+            Freq = Fdone + p.Kmax;
+            Fdirok = Fdone + 2 * p.Kmax;
+            CK(mal((void**)&Fdir, (size_t)p.Kmax * rm * sizeof(double)));
         }
         CK(mal((void**)&prog, (size_t)(5 * p.q + 2) * sizeof(int)));
         if (p.shard_ht() && !p.emul_ht) CK(mal((void**)&xfer, (size_t)2 * CH_BM * p.n * sizeof(S)));
@@ -366,7 +374,9 @@ struct Workspace {
         if (Fb) CK(fr(Fb));
         Fb = nullptr;
         if (Fdone) CK(fr(Fdone));
-        Fdone = nullptr;
+        Fdone = Freq = Fdirok = nullptr;
+        if (Fdir) CK(fr(Fdir));
+        Fdir = nullptr;
         CK(fr(prog));
         CK(fr(k1prof));
         CK(fr(lag));
@@ -533,7 +543,7 @@ int enqueue_groups(const Plan<S>& p, Workspace<S>& ws, cudaStream_t stream, bool
             CK(cudaEventCreate(&e));
             ev.push_back(e);
         }
-    if (ws.Fdone) CK(cudaMemsetAsync(ws.Fdone, 0, (size_t)p.Kmax * sizeof(int), stream));
+    if (ws.Fdone) CK(cudaMemsetAsync(ws.Fdone, 0, (size_t)3 * p.Kmax * sizeof(int), stream));
     if (qz) {
         CK(cudaEventRecord(ws.ev_qz[0], stream));  // workspace allocations visible to the side stream
         CK(cudaStreamWaitEvent(ws.side, ws.ev_qz[0], 0));
@@ -563,7 +573,10 @@ int enqueue_groups(const Plan<S>& p, Workspace<S>& ws, cudaStream_t stream, bool
                             p.helpers, ws.k1prof, getenv("HT_K1PROF_T") ? atoi(getenv("HT_K1PROF_T")) : -1,
                             p.hlag, p.gate, ws.lag};
             ca.Fg = ws.Fg;
-            ca.fst = (int64_t)2 * 64 * 64;
+            ca.fst = (int64_t)2 * (r <= 64 ? 64 * 64 : 128 * 128);
+            ca.Freq = ws.Freq;
+            ca.Fdirok = ws.Fdirok;
+            ca.Fdir = ws.Fdir;
             ca.rqu = p.rqu;
             ca.Fb = ws.Fb;
             ca.Fdone = ws.Fdone;
@@ -951,8 +964,21 @@ int run(int64_t n64, int64_t r64, S* H, int64_t ldh, S* T, int64_t ldt, S* Q, in
     const int Kmax = 1 + (n - 1 - 2) / r;
     // shared memory of a chase CTA; what the fixed buffers leave goes to staged strip rows
     // (HT_CHASE_SMEM_KB overrides; 224 KB measured no faster than 200 at r = 32, 64)
-    // K1's opposite reflector by RQ update (rqu.cuh, real 32 < r <= 64; HT_RQU=0: Householder RQ per step)
-    const int rqu = rqu_supported_r<S>(r) && !(getenv("HT_RQU") && atoi(getenv("HT_RQU")) == 0);
+    int dev = 0, smem_optin = 0, nsm = 0;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    // far-strip helpers per sweep: as many as fit next to the q sweeps, at most 3 (HT_HELPERS)
+    int helpers = std::max(0, std::min(3, nsm / q - 2));  // q=32: 2, q<=21: 3
+    if (getenv("HT_HELPERS")) helpers = std::max(0, std::min(3, atoi(getenv("HT_HELPERS"))));
+    if (getenv("HT_NO_HELPERS") || (1 + helpers) * q > nsm) helpers = 0;
+    // K1's opposite reflector by RQ update (rqu.cuh, real 32 < r <= 128; HT_RQU=0: Householder RQ per
+    // step).  Mode 2 (default with helpers): the sweep solves for the direction, a helper runs the
+    // RQ update; mode 1 (HT_RQU=1, or no helpers; r <= 64 only): the sweep runs the RQ update
+    int rqu_mode = 0;
+    if (rqu_supported_r<S>(r) && !(getenv("HT_RQU") && atoi(getenv("HT_RQU")) == 0))
+        rqu_mode = (helpers > 0 && !(getenv("HT_RQU") && atoi(getenv("HT_RQU")) == 1)) ? 2 : (r <= 64 ? 1 : 0);
+    const int rqu = rqu_mode != 0;
     const int chase_budget = (getenv("HT_CHASE_SMEM_KB") ? atoi(getenv("HT_CHASE_SMEM_KB")) : (rqu ? 224 : 200)) * 1024;
     const size_t chase_base = chase_smem_elems<S>(r, q, 0, rqu) * sizeof(S);
     const int strip_cap = (int)std::max<int64_t>(0, ((int64_t)chase_budget - (int64_t)chase_base) /
@@ -960,7 +986,7 @@ int run(int64_t n64, int64_t r64, S* H, int64_t ldh, S* T, int64_t ldt, S* Q, in
     const size_t chase_bytes = chase_smem_elems<S>(r, q, strip_cap, rqu) * sizeof(S);
     const bool acc_pre = accum_smem_bytes<S>(r, q, true) <= 200 * 1024;
     const size_t acc_bytes = accum_smem_bytes<S>(r, q, acc_pre);
-    const void* chase_fn = chase_kernel_for<S>(r);
+    const void* chase_fn = chase_kernel_for<S>(r, rqu);
     if (!chase_fn || q > 148) return refuse(HT_EUNSUPPORTED);  // one co-resident CTA per sweep
     // WY window blocks: real fp64, q in (16, 32] (QP = 32), single windows (no
     // K2m), 4 warp columns.  A step costs 2 w QP MACs per tile row instead of w^2 (w = q + r - 1), but
@@ -975,10 +1001,6 @@ int run(int64_t n64, int64_t r64, S* H, int64_t ldh, S* T, int64_t ldt, S* Q, in
     const int QPw = wy ? 32 : 0;
     const size_t ch_bytes = chain_bytes_rt<S>(WP, r, q, PM, QPw);
     const size_t mrg_bytes = PM > 1 ? merge_smem_bytes<S>(Wm, w) : 0;
-    int dev = 0, smem_optin = 0, nsm = 0;
-    CK(cudaGetDevice(&dev));
-    CK(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-    CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
     if (chase_bytes > (size_t)smem_optin || ch_bytes > (size_t)smem_optin || acc_bytes > (size_t)smem_optin ||
         mrg_bytes > (size_t)smem_optin)
         return refuse(HT_EUNSUPPORTED);
@@ -990,15 +1012,10 @@ int run(int64_t n64, int64_t r64, S* H, int64_t ldh, S* T, int64_t ldt, S* Q, in
                                 (int)accum_wy_smem_bytes<S>(r, q, QPw)));
 
     if (int rcp = chain_prepare<S>(WP)) return refuse(rcp);
-    // far-strip helpers per sweep: as many as fit next to the q sweeps, at most 3 (HT_HELPERS)
-    int helpers = std::max(0, std::min(3, nsm / q - 2));  // q=32: 2, q<=21: 3
-    if (getenv("HT_HELPERS")) helpers = std::max(0, std::min(3, atoi(getenv("HT_HELPERS"))));
-    if (getenv("HT_NO_HELPERS") || (1 + helpers) * q > nsm) helpers = 0;
     Plan<S> pl{n, r, q, WP, LDB, Kmax, strip_cap, chase_bytes, acc_bytes, chase_fn, H, ldh, T, ldt, Q, ldq, Z, ldz,
                std::max(8, nsm - (1 + helpers) * q)};
     pl.helpers = helpers;
-    // rqu 2 (default with helpers): the sweep solves for the direction, a helper runs the RQ update
-    pl.rqu = rqu ? ((helpers > 0 && !(getenv("HT_RQU") && atoi(getenv("HT_RQU")) == 1)) ? 2 : 1) : 0;
+    pl.rqu = rqu_mode;
     pl.wy = wy;
     pl.QP = QPw;
     pl.P = PM;

@@ -107,11 +107,15 @@ struct RQUCfg {
     static constexpr int RLD = MAXM + 1;           // row-major ld of R0 / Q0 in shared memory (odd)
     static constexpr int RPL = (MAXM + 31) / 32;   // chain rows per lane (warp 0)
     static constexpr int NPART = NT / MAXM;        // (A) row parts
-    static constexpr int QW = (MAXM + 31) / 32;    // Q column warps 1..QW
-    // shared memory besides R0 (which overlays the RQ ring): Q0, w parts, rotations (B) and (D)
-    static constexpr size_t extra = (size_t)MAXM * RLD + (size_t)NPART * MAXM + 4 * (size_t)MAXM + 2 +  // (+2: cs2 alignment)
-                                    (size_t)MAXM;  // x of the solve
-    static_assert(NPART >= 1 && NT >= 32 * (1 + QW), "RQU thread roles");
+    // MAXM <= 64: Q0 has its own buffer and warps 1..QW rotate it concurrently with the chain (D);
+    // MAXM = 128: R0 and Q0 do not both fit -- Q0 reuses R0's buffer after the hand-over of R~
+    static constexpr bool QCONC = MAXM <= 64;
+    static constexpr int QW = QCONC ? (MAXM + 31) / 32 : 0;
+    // shared memory besides R0 (which overlays the RQ ring / the B block): Q0 (QCONC), w parts,
+    // rotations (B) and (D) (+2: cs2 alignment), x of the solve, the column b
+    static constexpr size_t extra =
+        (QCONC ? (size_t)MAXM * RLD : 0) + (size_t)NPART * MAXM + 4 * (size_t)MAXM + 2 + 2 * (size_t)MAXM;
+    static_assert(NPART >= 1 && NT >= 32 * (1 + QW) && NT >= MAXM, "RQU thread roles");
 };
 
 // In: Rs = R0 (row-major, ld RLD, upper triangle rows/cols < m), Qs = Q0 (m x m), v (v[0] = 1),
@@ -210,7 +214,7 @@ __device__ __forceinline__ void rqu_direction(int m, const double* v, double tau
             if ((m - 1) % RPL == e) Sm = Sl[e];
         const double gamma = sqrt_nn(__shfl_sync(0xffffffffu, Sm, (m - 1) / RPL));
         __syncwarp();
-        asm volatile("bar.arrive 4, %0;" ::"r"(32 * (1 + QW)) : "memory");  // cs1 -> the Q warps
+        if constexpr (C::QCONC) asm volatile("bar.arrive 4, %0;" ::"r"(32 * (1 + QW)) : "memory");  // cs1 -> the Q warps
         // ---- (C) R0 G_0 ... G_{m-2} (upper Hessenberg), minus v gamma e_{m-1}^T
         // (loops unrolled by two with ping-pong register sets: a loop-carried copy of a prefetched
         // value made the compiler place the copy right behind the load, stalling on it)
@@ -297,16 +301,23 @@ __device__ __forceinline__ void rqu_direction(int m, const double* v, double tau
                     body(j - 1, xb, ab, ne);
                 }
             };
+            // rows >= 32 e drop out once j + 1 < 32 e
             if constexpr (RPL == 1) {
                 run(m - 2, 0, std::integral_constant<int, 1>());
-            } else {  // rows >= 32 drop out once j + 1 < 32
-                run(m - 2, 31, std::integral_constant<int, RPL>());
+            } else if constexpr (RPL == 2) {
+                run(m - 2, 31, std::integral_constant<int, 2>());
+                run(min(m - 2, 30), 0, std::integral_constant<int, 1>());
+            } else {
+                static_assert(RPL == 4, "MAXM 128");
+                run(m - 2, 95, std::integral_constant<int, 4>());
+                run(min(m - 2, 94), 63, std::integral_constant<int, 3>());
+                run(min(m - 2, 62), 31, std::integral_constant<int, 2>());
                 run(min(m - 2, 30), 0, std::integral_constant<int, 1>());
             }
         }
         if (lane == 0) sts64(rs0, carry[0]);
         tick(21);
-    } else if (warp <= QW) {
+    } else if (C::QCONC && warp <= QW) {
         // ---- Q~ = G'^T G^T Q0, one column per thread: forward rotations (B), then the chain's
         asm volatile("bar.sync 4, %0;" ::"r"(32 * (1 + QW)) : "memory");
         const int c = tid - 32;
@@ -348,7 +359,8 @@ __device__ __forceinline__ void rqu_direction(int m, const double* v, double tau
         }
     }
     __syncthreads();
-    for (int j = tid; j < MAXM; j += NT) cs2[2 * j] = RQU_SENTINEL;  // (before the next call's barriers)
+    if constexpr (C::QCONC)  // (before the next call's barriers; QCONC off: rqu_q_apply still reads them)
+        for (int j = tid; j < MAXM; j += NT) cs2[2 * j] = RQU_SENTINEL;
     tick(19);
 }
 
@@ -363,7 +375,8 @@ __device__ __forceinline__ void rqu_direction(int m, const double* v, double tau
 template <int NT, int MAXM>
 __device__ __forceinline__ bool rqu_solve(int m, const double* v, double tau, const double* Rs, const double* Qs,
                                           double* wpart, double* xs, double* uu, volatile int* okflag,
-                                          long long* pt = nullptr, long long* tc0 = nullptr) {
+                                          long long* pt = nullptr, long long* tc0 = nullptr,
+                                          const double* FWg = nullptr, bool hasB = false) {
     using C = RQUCfg<NT, MAXM>;
     constexpr int RLD = C::RLD, RPL = C::RPL, NPART = C::NPART, RPP = MAXM / NPART;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -452,13 +465,32 @@ __device__ __forceinline__ bool rqu_solve(int m, const double* v, double tau, co
         if (part < NPART) {
             double s0 = 0.0, s1 = 0.0;
             if (c < m) {
-                const int p0 = part * RPP, p1 = min(p0 + RPP, m);
-                int p = p0;
-                for (; p + 1 < p1; p += 2) {
-                    s0 = fma(Qs[p * RLD + c], xs[p], s0);
-                    s1 = fma(Qs[(p + 1) * RLD + c], xs[p + 1], s1);
+                if (FWg) {  // Q0 = diag(W, 1) (hasB) or W, W row-major (ld MAXM) in global memory
+                    const int f = hasB ? m - 1 : m;
+                    const int p0 = part * RPP, p1 = min(p0 + RPP, f);
+                    if (c < f) {
+                        int p = p0;
+                        for (; p + 3 < p1; p += 4) {  // (independent loads first)
+                            const double q0 = ldcg(FWg + p * MAXM + c), q1 = ldcg(FWg + (p + 1) * MAXM + c);
+                            const double q2 = ldcg(FWg + (p + 2) * MAXM + c), q3 = ldcg(FWg + (p + 3) * MAXM + c);
+                            s0 = fma(q0, xs[p], s0);
+                            s1 = fma(q1, xs[p + 1], s1);
+                            s0 = fma(q2, xs[p + 2], s0);
+                            s1 = fma(q3, xs[p + 3], s1);
+                        }
+                        for (; p < p1; ++p) s0 = fma(ldcg(FWg + p * MAXM + c), xs[p], s0);
+                    } else if (part == (m - 1) / RPP) {
+                        s0 = xs[m - 1];  // (hasB: the identity row / column)
+                    }
+                } else {
+                    const int p0 = part * RPP, p1 = min(p0 + RPP, m);
+                    int p = p0;
+                    for (; p + 1 < p1; p += 2) {
+                        s0 = fma(Qs[p * RLD + c], xs[p], s0);
+                        s1 = fma(Qs[(p + 1) * RLD + c], xs[p + 1], s1);
+                    }
+                    if (p < p1) s0 = fma(Qs[p * RLD + c], xs[p], s0);
                 }
-                if (p < p1) s0 = fma(Qs[p * RLD + c], xs[p], s0);
             }
             wpart[part * MAXM + c] = s0 + s1;
         }
@@ -472,6 +504,75 @@ __device__ __forceinline__ bool rqu_solve(int m, const double* v, double tau, co
     }
     rqu_tick(pt, tc0, 19);
     return ok;
+}
+
+// dst(p, c) = src[p MAXM + c] for p, c < f (upper: c >= p only), dst row-major with ld RLD; L2 reads,
+// eight rows in flight per thread (a load-store loop serialised one L2 latency per element).
+// All threads; no barrier.
+template <int NT, int MAXM>
+__device__ __forceinline__ void rqu_load_block(double* dst, const double* src, int f, bool upper) {
+    constexpr int RLD = RQUCfg<NT, MAXM>::RLD, NP = NT / MAXM;
+    const int c = threadIdx.x % MAXM, part = threadIdx.x / MAXM;
+    if (part >= NP || c >= f) return;
+    for (int p0 = part; p0 < f; p0 += 8 * NP) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int p = p0 + u * NP;
+            v[u] = (p < f && (!upper || c >= p)) ? ldcg(src + p * MAXM + c) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int p = p0 + u * NP;
+            if (p < f && (!upper || c >= p)) dst[p * RLD + c] = v[u];
+        }
+    }
+}
+
+// Q~ = G'^T G^T Q0 after the chain (QCONC off): one column per thread, all rotations in cs1 / cs2;
+// uu = Q~(0,:)^T.  All threads; ends with a barrier.
+template <int NT, int MAXM>
+__device__ __forceinline__ void rqu_q_apply(int m, double* Qs, const double* cs1, const double* cs2, double* uu) {
+    constexpr int RLD = RQUCfg<NT, MAXM>::RLD;
+    const int c = threadIdx.x;
+    if (c < m) {
+        const unsigned qa = opaque_u32(rq_smem_u32(Qs)) + 8u * c;
+        double carry = lds64(qa);
+        for (int i = 0; i <= m - 2; ++i) {
+            const double cc = cs1[2 * i], ss = cs1[2 * i + 1], yj = lds64(qa + 8u * (RLD * (i + 1)));
+            sts64(qa + 8u * (RLD * i), fma(cc, carry, -ss * yj));
+            carry = fma(ss, carry, cc * yj);
+        }
+        for (int j = m - 2; j >= 0; --j) {
+            const double cc = cs2[2 * j], ss = cs2[2 * j + 1], yj = lds64(qa + 8u * (RLD * j));
+            sts64(qa + 8u * (RLD * (j + 1)), fma(ss, yj, cc * carry));
+            carry = fma(cc, yj, -ss * carry);
+        }
+        sts64(qa, carry);
+        uu[c] = carry;
+    }
+    __syncthreads();
+}
+
+// Hand-over parts: FR = R~(1:m-1, 1:m-1) (upper triangle) and FW = (Q~ Z)(1:m-1, 1:m-1),
+// Z = I - sig z z^T, row-major with ld MAXM (0-based ranges)
+template <int NT, int MAXM>
+__device__ __forceinline__ void rqu_handoff_R(int m, const double* Rs, double* FR) {
+    constexpr int RLD = RQUCfg<NT, MAXM>::RLD, NW = NT / 32;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int i = 1 + warp; i < m; i += NW)
+        for (int c = i + lane; c < m; c += 32) FR[(i - 1) * MAXM + (c - 1)] = Rs[i * RLD + c];
+}
+template <int NT, int MAXM>
+__device__ __forceinline__ void rqu_handoff_W(int m, const double* Qs, const double* z, double sig, double* FW) {
+    constexpr int RLD = RQUCfg<NT, MAXM>::RLD, NW = NT / 32;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int i = 1 + warp; i < m; i += NW) {
+        double d = 0.0;
+        for (int c = lane; c < m; c += 32) d = fma(Qs[i * RLD + c], z[c], d);
+        d = warp_sum(d) * sig;
+        for (int c = 1 + lane; c < m; c += 32) FW[(i - 1) * MAXM + (c - 1)] = fma(-d, z[c], Qs[i * RLD + c]);
+    }
 }
 
 // Hand-over of step (j,k) to sweep j+1 (same k): FR = R~(1:m-1, 1:m-1) (upper triangle),

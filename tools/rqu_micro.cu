@@ -11,7 +11,10 @@
 
 #include "rqu.cuh"
 
-constexpr int NT = 256, MAXM = 64;
+#ifndef MAXM_
+#define MAXM_ 64
+#endif
+constexpr int NT = 256, MAXM = MAXM_;
 using CF = RQUCfg<NT, MAXM>;
 
 __global__ void micro(int mode, int m, int iters, const double* R0, const double* Q0, const double* v, double tau, double* Rout,
@@ -19,7 +22,7 @@ __global__ void micro(int mode, int m, int iters, const double* R0, const double
     extern __shared__ double sm[];
     constexpr int RLD = CF::RLD;
     double* Rs = sm;
-    double* Qs = Rs + MAXM * RLD;
+    double* Qs = Rs + (CF::QCONC ? MAXM * RLD : 0);
     double* wpart = Qs + MAXM * RLD;
     double* cs1 = wpart + CF::NPART * MAXM;
     double* cs2 = cs1 + 2 * MAXM;
@@ -35,14 +38,14 @@ __global__ void micro(int mode, int m, int iters, const double* R0, const double
         for (int e = threadIdx.x; e < m * m; e += NT) {
             const int p = e / m, c = e % m;
             Rs[p * RLD + c] = R0[p * m + c];
-            Qs[p * RLD + c] = Q0[p * m + c];
+            if (CF::QCONC) Qs[p * RLD + c] = Q0[p * m + c];
         }
         __syncthreads();
         tc = clock64();
         if (mode == 1) {
             rqu_direction<NT, MAXM>(m, vs, tau, Rs, Qs, wpart, cs1, cs2, uu, pt, &tc);
         } else {
-            rqu_solve<NT, MAXM>(m, vs, tau, Rs, Qs, wpart, xs, uu, &okf, pt, &tc);
+            rqu_solve<NT, MAXM>(m, vs, tau, Rs, Qs, wpart, xs, uu, &okf, pt, &tc, CF::QCONC ? nullptr : Q0, false);
             __syncthreads();
         }
     }
@@ -97,7 +100,7 @@ int main(int argc, char** argv) {
     cudaMemcpy(dR, R0.data(), m * m * 8, cudaMemcpyHostToDevice);
     cudaMemcpy(dQ, Q0.data(), m * m * 8, cudaMemcpyHostToDevice);
     cudaMemcpy(dv, v.data(), m * 8, cudaMemcpyHostToDevice);
-    const size_t smem = (2 * MAXM * CF::RLD + CF::NPART * MAXM + 4 * MAXM + 3 * MAXM) * 8;
+    const size_t smem = ((CF::QCONC ? 2 : 1) * MAXM * CF::RLD + CF::NPART * MAXM + 4 * MAXM + 3 * MAXM + 2) * 8;
     cudaFuncSetAttribute(micro, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     micro<<<1, NT, smem>>>(mode, m, iters, dR, dQ, dv, tau, dRo, dQo, du, dc);
     cudaError_t e = cudaDeviceSynchronize();
