@@ -60,6 +60,9 @@ struct ChaseArgs {
                         // triangular solve, the RQ update (hand-over) by the sweep's helper h = k mod H
     double* Fb = nullptr;  // rqu 2: the caught-up column b of step (j,k) per k (MAXM each)
     int* Fdone = nullptr;  // rqu 2: per k, j+1 once the hand-over of sweep j's step k is in Fg
+    // helper layout (nullptr: `helpers` per sweep): lay[t] = first helper index of sweep t (prefix
+    // sums, t <= qp), lay[qp + 1 + ticket] = (t << 8) | role of a CTA ticket (role 0: the sweep)
+    const int* lay = nullptr;
     int* Freq = nullptr;   // rqu 2, MAXM 128: per k, j+1 when sweep j's solve failed (direction requested)
     int* Fdirok = nullptr; // ... j+1 once the helper put Q~(1,:) in Fdir
     double* Fdir = nullptr;
@@ -168,6 +171,47 @@ __device__ __forceinline__ S larfg_reg(S xv, int m, S& tau, double& beta) {
     tau = S(1.0) - alpha * (pos ? -rs : rs);
     const S sc = fast_recip_s(alpha - S(beta));
     return lane == 0 ? S(1.0) : xv * sc;
+}
+
+// The same for m <= 32 EPL: lane l holds x[l + 32 e]; x and vout in shared memory (vout may alias x).
+// (warp_larfg's IEEE sqrt / divisions measured ~4k cycles at m = 64 on the step's chain.)
+template <typename S, int EPL>
+__device__ __forceinline__ void larfg_regn(int m, const S* x, S* vout, S& tau, double& beta) {
+    const int lane = threadIdx.x & 31;
+    S xv[EPL];
+    double s = 0.0;
+#pragma unroll
+    for (int e = 0; e < EPL; ++e) {
+        const int i = lane + 32 * e;
+        xv[e] = i < m ? x[i] : S(0.0);
+        if (i >= 1) s += abs2(xv[e]);
+    }
+    s = warp_sum(s);
+    const S alpha = shfl_idx(xv[0], 0);
+    __syncwarp();
+    if (s == 0.0 && im(alpha) == 0.0) {
+        tau = S(0.0);
+        beta = re(alpha);
+#pragma unroll
+        for (int e = 0; e < EPL; ++e) {
+            const int i = lane + 32 * e;
+            if (i < m) vout[i] = S(i == 0 ? 1.0 : 0.0);
+        }
+        __syncwarp();
+        return;
+    }
+    const double a2 = abs2(alpha) + s;
+    const double rs = fast_rsqrt(a2);
+    const bool pos = re(alpha) >= 0.0;
+    beta = pos ? -(a2 * rs) : a2 * rs;
+    tau = S(1.0) - alpha * (pos ? -rs : rs);
+    const S sc = fast_recip_s(alpha - S(beta));
+#pragma unroll
+    for (int e = 0; e < EPL; ++e) {
+        const int i = lane + 32 * e;
+        if (i < m) vout[i] = (i == 0) ? S(1.0) : xv[e] * sc;
+    }
+    __syncwarp();
 }
 
 // RQ thread layout.  Group A (threads [0, NA)) holds the m rows of C, group B (threads
@@ -613,7 +657,11 @@ __host__ __device__ inline size_t chase_smem_elems(int r, int qp, int strip_cap,
 // anyway); sweep j itself never reads those rows again.
 template <typename S, int NT, int MAXM, bool RQK>
 __device__ __forceinline__ void far_strip_helper(const ChaseArgs<S>& a, int t, int h, S* sm, const RQUBufs& rb) {
-    const int H = a.helpers;
+    // this sweep's helpers: H of them at hprog[hb ..]; the previous sweep's: Hp at hprog[hbp ..]
+    const int hb = a.lay ? __ldg(a.lay + t) : t * a.helpers;
+    const int H = a.lay ? __ldg(a.lay + t + 1) - hb : a.helpers;
+    const int hbp = t > 0 ? (a.lay ? __ldg(a.lay + t - 1) : (t - 1) * a.helpers) : 0;
+    const int Hp = t > 0 ? hb - hbp : 0;
     constexpr int RB = 64;  // row block: helper h owns blocks h, h+H, ... (relative to j1)
     const int n = a.n, r = a.r, qp = a.qp, j1 = a.j1, K = a.K;
     const int j = j1 + t;
@@ -719,14 +767,15 @@ __device__ __forceinline__ void far_strip_helper(const ChaseArgs<S>& a, int t, i
             if (ld_acquire(&a.prog[t]) < k + 1)
                 while (ld_relaxed(&a.prog[t]) < k + 1) {
                 }
-            if (t > 0) {
+            if (t > 0) {  // every helper of sweep t-1 through item k+1 (their row blocks may differ)
                 const int need = min(k + 2, kprev);
-                while (ld_relaxed(&hprog[(t - 1) * H + h]) < need) {
-                }
+                for (int hh = 0; hh < Hp; ++hh)
+                    while (ld_relaxed(&hprog[hbp + hh]) < need) {
+                    }
             }
             (void)ld_acquire(&a.prog[t]);
-            if (t > 0) (void)ld_acquire(&hprog[(t - 1) * H + h]);
-            if (a.trace) a.trace[((int64_t)qp * K + ((int64_t)t * H + h) * K + k) * 2] = gtimer();
+            asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
+            if (a.trace) a.trace[((int64_t)qp * K + ((int64_t)hb + h) * K + k) * 2] = gtimer();
         }
         __syncthreads();
         if (a.prof && tid == 0) {
@@ -749,52 +798,75 @@ __device__ __forceinline__ void far_strip_helper(const ChaseArgs<S>& a, int t, i
             __syncthreads();
             const S sig = zv[MAXM];
             if (!is_zero(sig)) {
-                // my row blocks intersected with the far rows [i4, i4 + nAf) (A) and [i4, i4 + nBf) (B)
+                // my row blocks intersected with the far rows [i4, i4 + nAf) (A) and [i4, i4 + nBf) (B);
+                // a block has at most 2 RB = NT / SPR rows: one row per thread.  Two blocks in flight
+                // (ping-pong registers): the next block's loads are issued before this block's dot.
                 const int nfar = max(nAf, nBf);
                 const int blk0 = (i4 - j1) / RB, blk1 = (i4 + nfar - 1 - j1) / RB;
-                for (int blk = blk0 + ((h - blk0 % H) + H) % H; blk <= blk1; blk += H) {
+                constexpr int RPT = (2 * RB + NT / SPR - 1) / (NT / SPR);  // rows per thread and block
+                const int bfirst = blk0 + ((h - blk0 % H) + H) % H;
+                const int nunits_ = bfirst <= blk1 ? ((blk1 - bfirst) / H + 1) * RPT : 0;
+                // unit u: block bfirst + (u / RPT) H, row tid / SPR + (u % RPT) NT / SPR of it
+                auto rowp = [&](int u, int64_t& ld) -> S* {  // my row of unit u (nullptr: none)
+                    const int blk = bfirst + (u / RPT) * H;
+                    const int eb = tid / SPR + (u % RPT) * (NT / SPR);
                     const int rlo = max(i4, j1 + blk * RB), rhi = min(i4 + nfar, j1 + (blk + 1) * RB);
                     const int nrA = max(0, min(rhi, i4 + nAf) - rlo), nrB = max(0, min(rhi, i4 + nBf) - rlo);
-                    const int nrows = nrA + nrB;
-                    for (int eb = tid / SPR; eb - tid / SPR < nrows; eb += NT / SPR) {
-                        const bool act = eb < nrows;
-                        const bool isA = eb < nrA;
-                        const int row = isA ? rlo + eb : rlo + (eb - nrA);
-                        S* gp = isA ? &IDX(a.A, a.lda, row, i1) : &IDX(a.B, a.ldb, row, i1);
-                        const int64_t ld = isA ? a.lda : a.ldb;
-                        S v[CPR];
-                        S s0 = S(0.0), s1 = S(0.0);
-                        if (act) {
-                            // all loads first: an FMA waiting on its load would hold back the
-                            // next load's issue (in-order issue), one memory latency per element
+                    if (u >= nunits_ || blk > blk1 || eb >= nrA + nrB) return nullptr;
+                    const bool isA = eb < nrA;
+                    ld = isA ? a.lda : a.ldb;
+                    return isA ? &IDX(a.A, a.lda, rlo + eb, i1) : &IDX(a.B, a.ldb, rlo + (eb - nrA), i1);
+                };
+                auto load = [&](const S* gp, int64_t ld, S* v) {
+                    // all loads first: an FMA waiting on its load would hold back the next load's
+                    // issue (in-order issue), one memory latency per element
+                    if (gp) {
 #pragma unroll
-                            for (int c = 0; c < CPR; ++c) v[c] = (c0 + c < m) ? ldcg(gp + (c0 + c) * ld) : S(0.0);
+                        for (int c = 0; c < CPR; ++c) v[c] = (c0 + c < m) ? ldcg(gp + (c0 + c) * ld) : S(0.0);
+                    }
+                };
+                auto finish = [&](S* gp, int64_t ld, const S* v) {  // (all threads: the shuffles)
+                    S s0 = S(0.0), s1 = S(0.0);
+                    if (gp) {
 #pragma unroll
-                            for (int c = 0; c < CPR; ++c) {
-                                if (c & 1) s1 = fma_s(v[c], zv[c0 + c], s1);
-                                else s0 = fma_s(v[c], zv[c0 + c], s0);
-                            }
-                        }
-                        S sdot = s0 + s1;
-                        if constexpr (SPR > 1) {
-#pragma unroll
-                            for (int o = 1; o < SPR; o <<= 1) sdot += shfl_xor(sdot, o);
-                        }
-                        if (act) {
-                            const S sv = sdot * sig;
-#pragma unroll
-                            for (int c = 0; c < CPR; ++c)
-                                if (c0 + c < m) gp[(c0 + c) * ld] = v[c] - sv * conjv(zv[c0 + c]);
+                        for (int c = 0; c < CPR; ++c) {
+                            if (c & 1) s1 = fma_s(v[c], zv[c0 + c], s1);
+                            else s0 = fma_s(v[c], zv[c0 + c], s0);
                         }
                     }
+                    S sdot = s0 + s1;
+                    if constexpr (SPR > 1) {
+#pragma unroll
+                        for (int o = 1; o < SPR; o <<= 1) sdot += shfl_xor(sdot, o);
+                    }
+                    if (gp) {
+                        const S sv = sdot * sig;
+#pragma unroll
+                        for (int c = 0; c < CPR; ++c)
+                            if (c0 + c < m) gp[(c0 + c) * ld] = v[c] - sv * conjv(zv[c0 + c]);
+                    }
+                };
+                const int nunits = nunits_;
+                S va[CPR], vb[CPR];
+                int64_t lda_ = 0, ldb_ = 0;
+                S* pa = rowp(0, lda_);
+                if (nunits > 0) load(pa, lda_, va);
+                for (int u = 0; u < nunits; u += 2) {
+                    S* pb = rowp(u + 1, ldb_);
+                    if (u + 1 < nunits) load(pb, ldb_, vb);
+                    finish(pa, lda_, va);
+                    if (u + 1 >= nunits) break;
+                    pa = rowp(u + 2, lda_);
+                    if (u + 2 < nunits) load(pa, lda_, va);
+                    finish(pb, ldb_, vb);
                 }
             }
         }
         __syncthreads();
         if (tid == 0) {
             __threadfence();
-            if (a.trace) a.trace[((int64_t)qp * K + ((int64_t)t * H + h) * K + k) * 2 + 1] = gtimer();
-            st_release(&hprog[t * H + h], k + 1);
+            if (a.trace) a.trace[((int64_t)qp * K + ((int64_t)hb + h) * K + k) * 2 + 1] = gtimer();
+            st_release(&hprog[hb + h], k + 1);
         }
         if constexpr (RQH) {
             // rqu 2: the RQ update of step (j,k) and its hand-over (unless the sweep did it: MAXM 64)
@@ -891,8 +963,16 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
     __shared__ int t_sh;
     if (threadIdx.x == 0) t_sh = atomicAdd(&a.prog[qp], 1);
     __syncthreads();
-    const int role = t_sh % (1 + a.helpers);  // tickets: sweep t, then its helpers
-    const int t = t_sh / (1 + a.helpers);
+    int role, t;  // tickets: sweep t, then its helpers
+    if (a.lay) {
+        if (t_sh >= qp + __ldg(a.lay + qp)) return;
+        const int code = __ldg(a.lay + qp + 1 + t_sh);
+        t = code >> 8;
+        role = code & 255;
+    } else {
+        role = t_sh % (1 + a.helpers);
+        t = t_sh / (1 + a.helpers);
+    }
     if (t >= qp) return;
     if (role > 0) {
         far_strip_helper<S, NT, MAXM, RQK>(a, t, role - 1, sm,
@@ -904,32 +984,35 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
     const int j = j1 + t;
     const int kcount = min(K, 2 + (n - j - 1) / r);
     const int kprev = (t > 0) ? min(K, 2 + (n - j) / r) : 0;
+    // the previous sweep's helpers: Hp of them at hprog[hbp ..] (at most 8)
+    const int hbp = t > 0 ? (a.lay ? __ldg(a.lay + t - 1) : (t - 1) * a.helpers) : 0;
+    const int Hp = t > 0 ? min(8, (a.lay ? __ldg(a.lay + t) : t * a.helpers) - hbp) : 0;
     int cur = 0;
     // K1 profile (HT_K1PROF): thread 0's cycle counts per phase, in shared memory (a register array
     // cost ~48 registers in every build)
     __shared__ long long pt[24];
-    __shared__ long long tc;
-    if (tid == 0) {
+    long long tc = clock64();  // (all threads: a tid-0-only branch here diverged warp 0 before its shuffles)
+    if (tid == 0)
         for (int i = 0; i < 24; ++i) pt[i] = 0;
-        tc = clock64();
-    }
 #define K1_TICK(slot)                         \
     do {                                      \
-        if (a.prof && tid == 0) {             \
+        if (a.prof) {                         \
             (void)*(volatile int*)&t_sh;      \
             const long long now_ = clock64(); \
-            pt[slot] += now_ - tc;            \
+            if (tid == 0) pt[slot] += now_ - tc; \
             tc = now_;                        \
         }                                     \
     } while (0)
     // sub-phase slot (16..23) that is also counted in its parent slot
 #define K1_SUB(slot, parent)                  \
     do {                                      \
-        if (a.prof && tid == 0) {             \
+        if (a.prof) {                         \
             (void)*(volatile int*)&t_sh;      \
             const long long now_ = clock64(); \
-            pt[slot] += now_ - tc;            \
-            pt[parent] += now_ - tc;          \
+            if (tid == 0) {                   \
+                pt[slot] += now_ - tc;        \
+                pt[parent] += now_ - tc;      \
+            }                                 \
             tc = now_;                        \
         }                                     \
     } while (0)
@@ -972,17 +1055,19 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
                 // (t-1, k+1) overlap rows >= b0(k-1)): the counters are read with relaxed loads
                 // issued together (one L2 round trip, not one per counter), then one acquire fence
                 const int need = min(k + 3, kprev), hneed = min(k + 2, kprev);
-                const int* hp = hprog + (t - 1) * a.helpers;
+                const int* hp = hprog + hbp;
                 int v = ld_relaxed(&a.prog[t - 1]);
-                int hv[3] = {hneed, hneed, hneed};
-                for (int h = 0; h < a.helpers && h < 3; ++h) hv[h] = ld_relaxed(hp + h);
+                int hv[8];
+#pragma unroll
+                for (int h = 0; h < 8; ++h) hv[h] = (h < Hp) ? ld_relaxed(hp + h) : hneed;
                 // rqu 2: sweep j-1's hand-over for window k (its helper's RQ update)
                 const bool fw = RQU_OK && a.rqu == 2 && min(j + (k + 1) * r, n) - (j + k * r + 1) >= 1 &&
                                 j + max(0, (k - 1) * r + 1) <= n;
                 int fv = fw ? ld_relaxed(&a.Fdone[k]) : j;
                 while (v < need) v = ld_relaxed(&a.prog[t - 1]);
                 K1_TICK(0);
-                for (int h = 0; h < a.helpers && h < 3; ++h)
+#pragma unroll
+                for (int h = 0; h < 8; ++h)
                     while (hv[h] < hneed) hv[h] = ld_relaxed(hp + h);
                 while (fv < j) fv = ld_relaxed(&a.Fdone[k]);
                 asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
@@ -1050,15 +1135,17 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
         K1_TICK(1);
         if constexpr (RQU_OK) {
             if (rqu) {  // sweep j-1's hand-over for window k (rqu.cuh), waited for before the RQ update
-                if (RQU64 && gen && j > 1) {
+                if (RQU64 && gen && j > 1) {  // thread: column c, rows part, part + NP, ... (no divisions)
                     const int f = hasB ? m - 1 : m;
                     const double* FR = a.Fg + (int64_t)k * a.fst;
                     const double* FW = FR + MAXM * MAXM;
-                    for (int e = tid; e < f * f; e += NT) {
-                        const int p = e / f, c = e - p * f;
-                        k1_ld(&Qs[p * RLD + c], FW + p * MAXM + c);
-                        if (c >= p) k1_ld(&Rs[p * RLD + c], FR + p * MAXM + c);
-                    }
+                    constexpr int NP = NT / RQM;
+                    const int c = tid % RQM;
+                    if (c < f)
+                        for (int p = tid / RQM; p < f; p += NP) {
+                            k1_ld(&Qs[p * RLD + c], FW + p * MAXM + c);
+                            if (c >= p) k1_ld(&Rs[p * RLD + c], FR + p * MAXM + c);
+                        }
                 }
                 k1_commit();
             }
@@ -1215,7 +1302,7 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
                         const S vl = larfg_reg(lane < m ? xcol[t + lane] : S(0.0), m, tq, beta);
                         if (lane < m) vq[lane] = vl;
                     } else {
-                        warp_larfg(m, xcol + t, vq, tq, beta);
+                        larfg_regn<S, (MAXM + 31) / 32>(m, xcol + t, vq, tq, beta);
                     }
                     if (lane == 0) {
                         scal[0] = tq;
@@ -1492,7 +1579,7 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
                         const S vl = larfg_reg(lane < m ? uu[lane] : S(0.0), m, sig, b2);
                         if (lane < m) vz[lane] = vl;
                     } else {
-                        warp_larfg(m, uu, vz, sig, b2);
+                        larfg_regn<S, (MAXM + 31) / 32>(m, uu, vz, sig, b2);
                     }
                     if (lane == 0) scal[2] = sig;
                 } else if (hasB && cu) {

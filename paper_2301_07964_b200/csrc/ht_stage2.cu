@@ -31,11 +31,13 @@ thread_local int64_t g_lag_checked = 0, g_lag_violations = 0;  // HT_LAG_CHECK (
 // chase launch, every ordering the wavefront protocol promises (lag 3 between
 // sweeps, the helpers' items behind their sweep and behind the previous sweep's helper) is checked:
 // a step / item must not start before the step / item it waits for has ended.
-void check_lag(const unsigned long long* tr, int n, int r, int qp, int j1, int K, int H) {
+void check_lag(const unsigned long long* tr, int n, int r, int qp, int j1, int K, const int* hoff) {
+    // hoff: first helper index of sweep t (prefix sums of the helper layout, t <= qp)
     auto send = [&](int t, int k) { return tr[((int64_t)t * K + k) * 2 + 1]; };
     auto sbeg = [&](int t, int k) { return tr[((int64_t)t * K + k) * 2]; };
-    auto hbeg = [&](int t, int h, int k) { return tr[((int64_t)qp * K + ((int64_t)t * H + h) * K + k) * 2]; };
-    auto hend = [&](int t, int h, int k) { return tr[((int64_t)qp * K + ((int64_t)t * H + h) * K + k) * 2 + 1]; };
+    auto hbeg = [&](int t, int h, int k) { return tr[((int64_t)qp * K + ((int64_t)hoff[t] + h) * K + k) * 2]; };
+    auto hend = [&](int t, int h, int k) { return tr[((int64_t)qp * K + ((int64_t)hoff[t] + h) * K + k) * 2 + 1]; };
+    auto H = [&](int t) { return hoff[t + 1] - hoff[t]; };
     for (int t = 0; t < qp; ++t) {
         const int j = j1 + t;
         const int kcount = std::min(K, 2 + (n - j - 1) / r);
@@ -45,18 +47,19 @@ void check_lag(const unsigned long long* tr, int n, int r, int qp, int j1, int K
                 const int need = std::min(k + 3, kprev), hneed = std::min(k + 2, kprev);
                 ++g_lag_checked;
                 if (sbeg(t, k) < send(t - 1, need - 1)) ++g_lag_violations;
-                for (int h = 0; h < H; ++h) {
+                for (int h = 0; h < H(t - 1); ++h) {
                     ++g_lag_checked;
                     if (sbeg(t, k) < hend(t - 1, h, hneed - 1)) ++g_lag_violations;
                 }
             }
-            for (int h = 0; h < H; ++h) {
+            for (int h = 0; h < H(t); ++h) {
                 ++g_lag_checked;
                 if (hbeg(t, h, k) < send(t, k)) ++g_lag_violations;
-                if (t > 0) {
-                    ++g_lag_checked;
-                    if (hbeg(t, h, k) < hend(t - 1, h, std::min(k + 2, kprev) - 1)) ++g_lag_violations;
-                }
+                if (t > 0)
+                    for (int hh = 0; hh < H(t - 1); ++hh) {  // every helper of the previous sweep
+                        ++g_lag_checked;
+                        if (hbeg(t, h, k) < hend(t - 1, hh, std::min(k + 2, kprev) - 1)) ++g_lag_violations;
+                    }
             }
         }
     }
@@ -227,6 +230,34 @@ size_t nccl_count(size_t elems) { return elems * (sizeof(S) / sizeof(double)); }
         }                                                                         \
     } while (0)
 
+// Helper layout of a group of qp sweeps (ChaseArgs::lay): Htot far-strip helper CTAs distributed
+// over the sweeps in proportion to (qp - 1 - t) + F -- sweep t's far strip (band rows above b0(k))
+// is (qp - 1 - t) r rows in steady state (i4 = j1 + 1 + (k + t - qp + 1) r), and F stands for the
+// RQ-update work every sweep's helpers share; at least 1 and at most 8 per sweep, allocated greedily
+// (max-min).  Uniform (Htot / qp each) when bal == false.
+std::vector<int> helper_layout(int qp, int Htot, bool bal, double F) {
+    std::vector<int> Hs(qp, Htot / std::max(1, qp));
+    if (bal && qp > 1 && Htot >= qp) {  // greedy: the next helper to the sweep with the largest load per helper
+        std::fill(Hs.begin(), Hs.end(), 1);
+        for (int e = qp; e < Htot; ++e) {
+            int best = -1;
+            double bl = -1.0;
+            for (int t = 0; t < qp; ++t) {
+                const double l = ((qp - 1 - t) + F) / Hs[t];
+                if (Hs[t] < 8 && l > bl) bl = l, best = t;
+            }
+            if (best < 0) break;
+            ++Hs[best];
+        }
+    }
+    std::vector<int> lay(qp + 1);
+    lay[0] = 0;
+    for (int t = 0; t < qp; ++t) lay[t + 1] = lay[t] + Hs[t];
+    for (int t = 0; t < qp; ++t)
+        for (int role = 0; role <= Hs[t]; ++role) lay.push_back((t << 8) | role);
+    return lay;
+}
+
 template <typename S>
 struct Plan {
     int n, r, q, WP, LDB, Kmax, strip_cap;
@@ -262,12 +293,14 @@ struct Plan {
     int wy = 0, QP = 0;      // WY window blocks (chain.cuh ChainParams::wy; accum_wy_kernel)
     int hlag = 1;          // helper row split (ChaseArgs::hlag): 0 for r >= 32 (HT_HELPER_LAG overrides)
     int rqu = 0;           // K1 opposite reflector by RQ update (rqu.cuh; HT_RQU=0 disables)
+    int hbal = 0;          // helpers distributed over the sweeps by far-strip load (helper_layout)
+    double hF = 10.0;      // ... its per-sweep constant, in far-strip rows / r (HT_HELPER_F)
     size_t mrg_bytes = 0;
     const unsigned long long* gate = nullptr;  // device verdict words of the input check (nullptr: none)
     bool is_root() const { return comm == nullptr || rank == root; }
     bool qz() const { return Q || Z; }
     bool same(const Plan& o) const {
-        return n == o.n && r == o.r && q == o.q && strip_cap == o.strip_cap && helpers == o.helpers && P == o.P && qz_late == o.qz_late && qz_groups == o.qz_groups && far_side == o.far_side && wy == o.wy && hlag == o.hlag && rqu == o.rqu && G == o.G && emul_ht == o.emul_ht && gate == o.gate && H == o.H && ldh == o.ldh &&
+        return n == o.n && r == o.r && q == o.q && strip_cap == o.strip_cap && helpers == o.helpers && P == o.P && qz_late == o.qz_late && qz_groups == o.qz_groups && far_side == o.far_side && wy == o.wy && hlag == o.hlag && rqu == o.rqu && hbal == o.hbal && hF == o.hF && G == o.G && emul_ht == o.emul_ht && gate == o.gate && H == o.H && ldh == o.ldh &&
                T == o.T && ldt == o.ldt && Q == o.Q && ldq == o.ldq && Z == o.Z && ldz == o.ldz;
     }
 };
@@ -283,6 +316,9 @@ inline int64_t mcatch_st(int q, int r) { return (int64_t)(q + r - 1) * mcatch_ld
 template <typename S>
 struct Workspace {
     S *U[NUV] = {}, *V[NUV] = {}, *MU[NUV] = {}, *MV[NUV] = {}, *Zr = nullptr, *Qr = nullptr, *Tr = nullptr, *Mg = nullptr;
+    int* lay = nullptr;    // helper layouts (helper_layout) of the full groups and of the last group
+    std::vector<int> lay_host;
+    int lay_last = 0;      // offset of the last group's layout
     double* Fg = nullptr;  // RQ-update hand-over (Kmax x 2 x 64 x 64), kept across groups
     double* Fb = nullptr;  // rqu 2: caught-up column b per window (Kmax x MAXM)
     int* Fdone = nullptr;  // rqu 2: hand-over generation per window (Kmax)
@@ -320,6 +356,16 @@ struct Workspace {
         CK(mal((void**)&Qr, rec));
         CK(mal((void**)&Tr, tf));
         if (chase_dense_catchup<S>(p.r)) CK(mal((void**)&Mg, (size_t)p.Kmax * mcatch_st(p.q, p.r) * sizeof(S)));
+        if (p.helpers > 0) {  // helper layouts: full groups (qp = q) and the last group
+            const int ngroups = (p.n - 2 + p.q - 1) / p.q;
+            const int qlast = std::min(p.q, p.n - 1 - (1 + (ngroups - 1) * p.q));
+            lay_host = helper_layout(p.q, p.helpers * p.q, p.hbal != 0, p.hF);
+            lay_last = (int)lay_host.size();
+            const std::vector<int> l2 = helper_layout(qlast, p.helpers * qlast, p.hbal != 0, p.hF);
+            lay_host.insert(lay_host.end(), l2.begin(), l2.end());
+            CK(mal((void**)&lay, lay_host.size() * sizeof(int)));
+            CK(cudaMemcpyAsync(lay, lay_host.data(), lay_host.size() * sizeof(int), cudaMemcpyHostToDevice, stream));
+        }
         const size_t rm = p.r <= 64 ? 64 : 128;  // MAXM of the RQ update
         if (p.rqu) CK(mal((void**)&Fg, (size_t)p.Kmax * 2 * rm * rm * sizeof(double)));
         if (p.rqu == 2) {
@@ -371,6 +417,8 @@ struct Workspace {
         Mg = nullptr;
         if (Fg) CK(fr(Fg));
         Fg = nullptr;
+        if (lay) CK(fr(lay));
+        lay = nullptr;
         if (Fb) CK(fr(Fb));
         Fb = nullptr;
         if (Fdone) CK(fr(Fdone));
@@ -411,7 +459,7 @@ void print_k1prof(const long long* h) {
         if (i != 11 && h[i]) fprintf(stderr, " %s=%.0f", nm[i], h[i] / steps);
     fprintf(stderr, " all=%.0f\n", tot / steps);
     // sub-phases (parts of the slots above): the RQ update (rqu.cuh)
-    const char* sn[8] = {"rqu_loadwait", "rqu_A", "rqu_BC|solve", "rqu_D|Qx", "rqu_handoff", "rqu_Dchain", "S4_QB_tid0", "S4_T_tidNT/2"};
+    const char* sn[8] = {"rqu_loadwait", "rqu_A", "rqu_BC|solve", "rqu_D|Qx", "rqu_handoff", "s21", "S4_QB_tid0", "S4_T_tidNT/2"};
     bool any = false;
     for (int i = 16; i < 24; ++i) any |= h[i] != 0;
     if (any) {
@@ -578,6 +626,7 @@ int enqueue_groups(const Plan<S>& p, Workspace<S>& ws, cudaStream_t stream, bool
             ca.Fdirok = ws.Fdirok;
             ca.Fdir = ws.Fdir;
             ca.rqu = p.rqu;
+            ca.lay = ws.lay ? ws.lay + (qp == q ? 0 : ws.lay_last) : nullptr;
             ca.Fb = ws.Fb;
             ca.Fdone = ws.Fdone;
             const size_t lag_elems = (size_t)2 * qp * K * (1 + p.helpers);
@@ -588,7 +637,7 @@ int enqueue_groups(const Plan<S>& p, Workspace<S>& ws, cudaStream_t stream, bool
                 std::vector<unsigned long long> h(lag_elems);
                 CK(cudaMemcpyAsync(h.data(), ws.lag, lag_elems * sizeof(unsigned long long), cudaMemcpyDeviceToHost, stream));
                 CK(cudaStreamSynchronize(stream));
-                check_lag(h.data(), n, r, qp, j1, K, p.helpers);
+                check_lag(h.data(), n, r, qp, j1, K, ws.lay_host.data() + (qp == q ? 0 : ws.lay_last));
             }
         }
         if (p.comm && (qz || p.shard_ht())) {  // the group's reflectors (2 qp K (r+1) scalars) to every rank
@@ -1016,6 +1065,10 @@ int run(int64_t n64, int64_t r64, S* H, int64_t ldh, S* T, int64_t ldt, S* Q, in
                std::max(8, nsm - (1 + helpers) * q)};
     pl.helpers = helpers;
     pl.rqu = rqu_mode;
+    // greedy by load (measured config 4 chase 5.68 -> 5.36 s at F = 8..12; config-5 shape n = 16384
+    // 17.3 -> 15.4 s at F = 8); HT_HELPER_BAL=0: uniform
+    pl.hbal = !(getenv("HT_HELPER_BAL") && atoi(getenv("HT_HELPER_BAL")) == 0);
+    if (getenv("HT_HELPER_F")) pl.hF = atof(getenv("HT_HELPER_F"));
     pl.wy = wy;
     pl.QP = QPw;
     pl.P = PM;

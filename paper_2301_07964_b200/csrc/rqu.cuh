@@ -124,10 +124,12 @@ struct RQUCfg {
 // even slots at entry (initialise once; every call restores it).
 // (profile: thread 0's cycles into K1 sub-slot `slot`, also counted in slot 6)
 __device__ __forceinline__ void rqu_tick(long long* pt, long long* tc0, int slot) {
-    if (pt && threadIdx.x == 0) {
+    if (pt) {  // (all threads: tc0 is per thread; only thread 0 records)
         const long long now = clock64();
-        pt[slot] += now - *tc0;
-        pt[6] += now - *tc0;
+        if (threadIdx.x == 0) {
+            pt[slot] += now - *tc0;
+            pt[6] += now - *tc0;
+        }
         *tc0 = now;
     }
 }
