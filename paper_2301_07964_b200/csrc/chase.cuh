@@ -847,8 +847,16 @@ __device__ __forceinline__ void far_strip_helper(const ChaseArgs<S>& a, int t, i
                     }
                 };
                 const int nunits = nunits_;
-                S va[CPR], vb[CPR];
+                S va[CPR];
                 int64_t lda_ = 0, ldb_ = 0;
+                if constexpr (sizeof(S) > 8) {  // complex: one row in flight (two spilled registers)
+                    for (int u = 0; u < nunits; ++u) {
+                        S* pa = rowp(u, lda_);
+                        load(pa, lda_, va);
+                        finish(pa, lda_, va);
+                    }
+                } else {
+                S vb[CPR];
                 S* pa = rowp(0, lda_);
                 if (nunits > 0) load(pa, lda_, va);
                 for (int u = 0; u < nunits; u += 2) {
@@ -859,6 +867,7 @@ __device__ __forceinline__ void far_strip_helper(const ChaseArgs<S>& a, int t, i
                     pa = rowp(u + 2, lda_);
                     if (u + 2 < nunits) load(pa, lda_, va);
                     finish(pb, ldb_, vb);
+                }
                 }
             }
         }
