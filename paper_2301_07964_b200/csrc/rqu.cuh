@@ -386,10 +386,13 @@ __device__ __forceinline__ bool rqu_solve(int m, const double* v, double tau, co
     rqu_tick(pt, tc0, 17);
     if (warp == 0) {
         const unsigned rs0 = opaque_u32(rq_smem_u32(Rs));
+        // rows p = RPL lane + e (consecutive): one lane's RPL columns per step of the back
+        // substitution -- the lead lane solves its RPL x RPL triangle, one broadcast, then every
+        // lane updates its rows for RPL columns (half / a quarter of the shuffle chain)
         double w[RPL], rhs[RPL], rinv[RPL], u[RPL];
 #pragma unroll
         for (int e = 0; e < RPL; ++e) {
-            const int p = lane + 32 * e;
+            const int p = RPL * lane + e;
             double x = 0.0;
             if (p < m) {
 #pragma unroll
@@ -402,37 +405,47 @@ __device__ __forceinline__ bool rqu_solve(int m, const double* v, double tau, co
             rinv[e] = row ? fast_rcp(lds64(rs0 + 8u * (p * RLD + p))) : 0.0;  // (0 pivot: inf -> fallback)
             u[e] = 0.0;
         }
-        // back substitution over columns i = m-1 .. 1 (column i's entries of my rows prefetched)
-        double ca[RPL], cb[RPL];
-        auto load = [&](int i, double* col) {
+        // col[e][f] = R(RPL lane + e, RPL L + f) for the step's lane-block L (0 outside rows 1..m-1
+        // and below the diagonal)
+        double ca[RPL][RPL], cb[RPL][RPL];
+        auto load = [&](int L, double (*col)[RPL]) {
 #pragma unroll
-            for (int e = 0; e < RPL; ++e) {
-                const int p = lane + 32 * e;
-                col[e] = lds64_if(p >= 1 && p < i, rs0 + 8u * (p * RLD + i));
-            }
+            for (int e = 0; e < RPL; ++e)
+#pragma unroll
+                for (int f = 0; f < RPL; ++f) {
+                    const int p = RPL * lane + e, c = RPL * L + f;
+                    col[e][f] = lds64_if(p >= 1 && p < c && c < m, rs0 + 8u * (p * RLD + c));
+                }
         };
-        auto body = [&](int i, const double* col) {
-            const int L = i & 31, eL = i >> 5;
-            double ui = rhs[0] * rinv[0];
+        auto body = [&](int L, double (*col)[RPL]) {
+            double ub[RPL];  // the lead's solve of its triangle (every lane computes its own; lane L's is used)
 #pragma unroll
-            for (int e = 1; e < RPL; ++e)
-                if (eL == e) ui = rhs[e] * rinv[e];
-            ui = __shfl_sync(0xffffffffu, ui, L);
+            for (int e = RPL - 1; e >= 0; --e) {
+                double t = rhs[e];
 #pragma unroll
-            for (int e = 0; e < RPL; ++e) {
-                const int p = lane + 32 * e;
-                if (p == i) u[e] = ui;
-                rhs[e] = fma(-col[e], ui, rhs[e]);
+                for (int f = e + 1; f < RPL; ++f) t = fma(-col[e][f], ub[f], t);
+                ub[e] = t * rinv[e];
             }
+#pragma unroll
+            for (int f = 0; f < RPL; ++f) ub[f] = __shfl_sync(0xffffffffu, ub[f], L);
+            if (lane == L) {
+#pragma unroll
+                for (int e = 0; e < RPL; ++e) u[e] = ub[e];
+            }
+#pragma unroll
+            for (int e = 0; e < RPL; ++e)
+#pragma unroll
+                for (int f = 0; f < RPL; ++f) rhs[e] = fma(-col[e][f], ub[f], rhs[e]);
         };
-        if (m >= 2) load(m - 1, ca);
+        const int Ltop = (m - 1) / RPL;
+        if (m >= 2) load(Ltop, ca);
         __syncwarp();  // (converged before the shuffle chain: a diverged warp takes BRA.DIV's slow shuffles)
-        for (int i = m - 1; i >= 1; i -= 2) {
-            if (i - 1 >= 1) load(i - 1, cb);
-            body(i, ca);
-            if (i - 1 < 1) break;
-            if (i - 2 >= 1) load(i - 2, ca);
-            body(i - 1, cb);
+        for (int L = Ltop; L >= 0; L -= 2) {
+            if (L - 1 >= 0) load(L - 1, cb);
+            body(L, ca);
+            if (L - 1 < 0) break;
+            if (L - 2 >= 0) load(L - 2, ca);
+            body(L - 1, cb);
         }
         double dot = 0.0;
 #pragma unroll
@@ -448,7 +461,7 @@ __device__ __forceinline__ bool rqu_solve(int m, const double* v, double tau, co
         }
 #pragma unroll
         for (int e = 0; e < RPL; ++e) {
-            const int p = lane + 32 * e;
+            const int p = RPL * lane + e;
             if (p >= 1 && p < m) {
                 const double xp = w0 * u[e];
                 xs[p] = xp;
