@@ -66,6 +66,11 @@ struct ChaseArgs {
     int* Freq = nullptr;   // rqu 2, MAXM 128: per k, j+1 when sweep j's solve failed (direction requested)
     int* Fdirok = nullptr; // ... j+1 once the helper put Q~(1,:) in Fdir
     double* Fdir = nullptr;
+    // rqu 2, MAXM 64: the sweep runs the RQ update itself (as after a failed solve) on the steps k
+    // with (k num) mod den < num -- a share num/den of the hand-overs moves from the helpers (the
+    // critical resource at config 4: a helper's strip item plus its hand-overs outlast a sweep
+    // step) to the sweep (HT_RQU_SELF=num/den; 0/1: none)
+    int rqu_self_num = 0, rqu_self_den = 1;
 };
 
 // shared-memory buffers of the RQ update (chase_kernel carves them; helpers use them too)
@@ -1492,11 +1497,13 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
                     if constexpr (RQU64) {
                         const double* vd = reinterpret_cast<const double*>(vq);
                         double* ud = reinterpret_cast<double*>(uu);
-                        if (a.rqu == 2)
+                        const bool self = a.rqu == 2 && (k * a.rqu_self_num) % a.rqu_self_den < a.rqu_self_num;
+                        if (a.rqu == 2 && !self)
                             rqu_fallback = !rqu_solve<NT, MAXM>(m, vd, re(tau), Rs, Qs, wpart, xs, ud, &rqu_ok,
                                                                 a.prof ? pt : nullptr, &tc);
-                        if (a.rqu != 2 || rqu_fallback)
+                        if (a.rqu != 2 || rqu_fallback || self)
                             rqu_direction<NT, MAXM>(m, vd, re(tau), Rs, Qs, wpart, cs1, cs2, ud, a.prof ? pt : nullptr, &tc);
+                        if (self) rqu_fallback = true;  // the hand-over below, Fdone at the release
                     } else if constexpr (RQU128) {  // Q0 read from the hand-over in L2
                         const double* vd = reinterpret_cast<const double*>(vq);
                         double* ud = reinterpret_cast<double*>(uu);

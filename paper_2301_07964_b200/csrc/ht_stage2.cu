@@ -295,12 +295,13 @@ struct Plan {
     int rqu = 0;           // K1 opposite reflector by RQ update (rqu.cuh; HT_RQU=0 disables)
     int hbal = 0;          // helpers distributed over the sweeps by far-strip load (helper_layout)
     double hF = 10.0;      // ... its per-sweep constant, in far-strip rows / r (HT_HELPER_F)
+    int rqu_self_num = 0, rqu_self_den = 1;  // rqu 2: share of the hand-overs the sweep runs (HT_RQU_SELF)
     size_t mrg_bytes = 0;
     const unsigned long long* gate = nullptr;  // device verdict words of the input check (nullptr: none)
     bool is_root() const { return comm == nullptr || rank == root; }
     bool qz() const { return Q || Z; }
     bool same(const Plan& o) const {
-        return n == o.n && r == o.r && q == o.q && strip_cap == o.strip_cap && helpers == o.helpers && P == o.P && qz_late == o.qz_late && qz_groups == o.qz_groups && far_side == o.far_side && wy == o.wy && hlag == o.hlag && rqu == o.rqu && hbal == o.hbal && hF == o.hF && G == o.G && emul_ht == o.emul_ht && gate == o.gate && H == o.H && ldh == o.ldh &&
+        return n == o.n && r == o.r && q == o.q && strip_cap == o.strip_cap && helpers == o.helpers && P == o.P && qz_late == o.qz_late && qz_groups == o.qz_groups && far_side == o.far_side && wy == o.wy && hlag == o.hlag && rqu == o.rqu && hbal == o.hbal && hF == o.hF && rqu_self_num == o.rqu_self_num && rqu_self_den == o.rqu_self_den && G == o.G && emul_ht == o.emul_ht && gate == o.gate && H == o.H && ldh == o.ldh &&
                T == o.T && ldt == o.ldt && Q == o.Q && ldq == o.ldq && Z == o.Z && ldz == o.ldz;
     }
 };
@@ -629,6 +630,8 @@ int enqueue_groups(const Plan<S>& p, Workspace<S>& ws, cudaStream_t stream, bool
             ca.lay = ws.lay ? ws.lay + (qp == q ? 0 : ws.lay_last) : nullptr;
             ca.Fb = ws.Fb;
             ca.Fdone = ws.Fdone;
+            ca.rqu_self_num = p.rqu_self_num;
+            ca.rqu_self_den = p.rqu_self_den;
             const size_t lag_elems = (size_t)2 * qp * K * (1 + p.helpers);
             if (ws.lag) CK(cudaMemsetAsync(ws.lag, 0, lag_elems * sizeof(unsigned long long), stream));
             void* kargs[] = {&ca};
@@ -638,6 +641,21 @@ int enqueue_groups(const Plan<S>& p, Workspace<S>& ws, cudaStream_t stream, bool
                 CK(cudaMemcpyAsync(h.data(), ws.lag, lag_elems * sizeof(unsigned long long), cudaMemcpyDeviceToHost, stream));
                 CK(cudaStreamSynchronize(stream));
                 check_lag(h.data(), n, r, qp, j1, K, ws.lay_host.data() + (qp == q ? 0 : ws.lay_last));
+                // HT_TRACE_DUMP=file (with HT_LAG_CHECK=1): the raw stamps of the group starting at
+                // HT_TRACE_J1 (default 1) and the helper offsets, for tools/trace_path.py
+                const char* td = getenv("HT_TRACE_DUMP");
+                const int tj1 = getenv("HT_TRACE_J1") ? atoi(getenv("HT_TRACE_J1")) : 1;
+                if (td && j1 == tj1)
+                    if (FILE* f = fopen(td, "wb")) {
+                        const int hdr[6] = {n, r, qp, j1, K, p.helpers};
+                        fwrite(hdr, sizeof(int), 6, f);
+                        const int* ho = ws.lay_host.data() + (qp == q ? 0 : ws.lay_last);
+                        std::vector<int> hoff(qp + 1, 0);
+                        for (int t = 0; t <= qp; ++t) hoff[t] = ws.lay ? ho[t] : t * p.helpers;
+                        fwrite(hoff.data(), sizeof(int), qp + 1, f);
+                        fwrite(h.data(), sizeof(unsigned long long), lag_elems, f);
+                        fclose(f);
+                    }
             }
         }
         if (p.comm && (qz || p.shard_ht())) {  // the group's reflectors (2 qp K (r+1) scalars) to every rank
@@ -1069,6 +1087,13 @@ int run(int64_t n64, int64_t r64, S* H, int64_t ldh, S* T, int64_t ldt, S* Q, in
     // 17.3 -> 15.4 s at F = 8); HT_HELPER_BAL=0: uniform
     pl.hbal = !(getenv("HT_HELPER_BAL") && atoi(getenv("HT_HELPER_BAL")) == 0);
     if (getenv("HT_HELPER_F")) pl.hF = atof(getenv("HT_HELPER_F"));
+    if (const char* e = getenv("HT_RQU_SELF")) {
+        int a = 0, b = 1;
+        if (sscanf(e, "%d/%d", &a, &b) == 2 && b > 0 && a >= 0 && a <= b) {
+            pl.rqu_self_num = a;
+            pl.rqu_self_den = b;
+        }
+    }
     pl.wy = wy;
     pl.QP = QPw;
     pl.P = PM;

@@ -1,7 +1,8 @@
 """GPU parity of K1's RQ-update paths (rqu.cuh; real 32 < r <= 128).
 
 * modes: HT_RQU=0 (Householder RQ per step), 1 (the sweep runs the RQ update, r <= 64),
-  2 (default: the sweep solves for the direction, a helper runs the RQ update);
+  2 (default: the sweep solves for the direction, a helper runs the RQ update), and mode 2 with a
+  share of the hand-overs run by the sweep itself (HT_RQU_SELF=num/den, m <= 64);
 * the fallbacks of a singular R22 (exact zeros on T's diagonal reach the blocks): the sweep's own
   Givens chain at m <= 64, the helper's early answer (Freq / Fdirok) at m = 128 -- checked on
   invariants (several results are correct for a singular T, reading c9);
@@ -33,7 +34,8 @@ def env(request):
 
 
 MODES = [{"HT_RQU": "0"}, {"HT_RQU": "1"}, {"HT_RQU": "2"}, {"HT_HELPER_BAL": "0"},
-         {"HT_HELPER_BAL": "1", "HT_HELPER_F": "2"}, {"HT_NO_HELPERS": "1"}, {"HT_NO_GRAPH": "1"}]
+         {"HT_HELPER_BAL": "1", "HT_HELPER_F": "2"}, {"HT_NO_HELPERS": "1"}, {"HT_NO_GRAPH": "1"},
+         {"HT_RQU_SELF": "1/2"}, {"HT_RQU_SELF": "2/3"}, {"HT_RQU_SELF": "1/1"}]
 
 
 @pytest.mark.parametrize("env", MODES, indirect=True, ids=lambda d: ",".join(f"{k}={v}" for k, v in d.items()))
@@ -44,7 +46,7 @@ def test_rqu_mode_parity(env, n, r, q):
     check_parity(H, T, r, q=q)
 
 
-@pytest.mark.parametrize("env", [{}, {"HT_RQU": "1"}], indirect=True, ids=lambda d: ",".join(f"{k}={v}" for k, v in d.items()) or "default")
+@pytest.mark.parametrize("env", [{}, {"HT_RQU": "1"}, {"HT_RQU_SELF": "1/2"}], indirect=True, ids=lambda d: ",".join(f"{k}={v}" for k, v in d.items()) or "default")
 @pytest.mark.parametrize("n,r,q,every", [(400, 64, 32, 4), (300, 48, 16, 2), (500, 128, 32, 4), (380, 128, 9, 3)])
 def test_rqu_singular_T_fallbacks(env, n, r, q, every):
     # exact zeros on T's diagonal: R22 of the hand-over is singular in many steps, so the solve
