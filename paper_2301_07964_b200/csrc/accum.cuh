@@ -11,6 +11,7 @@
 // [l*LDB + c], rows/cols >= w_k zero (so padded DMMA K-steps contribute nothing).
 #pragma once
 #include "scalar.cuh"
+#include "chain.cuh"  // chain_ldb / chain_wy_ldy: the block strides the chains read
 
 template <typename S>
 struct AccumArgs {
@@ -211,7 +212,7 @@ __global__ void __launch_bounds__(NT) accum_wy_kernel(AccumWYArgs<S> a) {
     if (input_rejected(a.gate)) return;
     extern __shared__ __align__(16) unsigned char smraw[];
     const int n = a.n, r = a.r, qp = a.qp, j1 = a.j1, K = a.K, WP = a.WP, QP = a.QP;
-    const int LDY = QP + 8, LDB = WP + 8;
+    const int LDY = chain_wy_ldy<S>(QP), LDB = chain_ldb<S>(WP);
     const int k = blockIdx.x;
     const bool isV = blockIdx.y != 0;
     const S* R = isV ? a.Zr : a.Qr;

@@ -26,6 +26,21 @@
 #define IDX(p, ld, i, j) (p)[((int64_t)(i) - 1) + ((int64_t)(j) - 1) * (int64_t)(ld)]
 #endif
 
+// Shared-memory strides of X (tile rows per column) and of the block rows.  An m8n8k4 fragment load
+// has lane & 3 along k (the stride) and lane >> 2 along the tile row / block column (contiguous); a
+// 64-bit load is served per half-warp (4 k x 4 rows), a 128-bit load per quarter-warp (4 k x 2
+// rows), so the stride must be 4 or 12 mod 16 doubles (real) and 2 or 6 mod 8 elements (complex):
+// stride 8 mod 16 put k and k + 2 on the same banks (two-way conflicts on every fragment load,
+// four-way for complex).  HT_CHAIN_PAD=8 restores the old strides (A/B builds).
+#ifndef HT_CHAIN_PAD
+#define HT_CHAIN_PAD 0
+#endif
+template <typename S>
+__host__ __device__ constexpr int chain_pad() { return HT_CHAIN_PAD ? HT_CHAIN_PAD : (sizeof(S) == 8 ? 4 : 2); }
+
+template <typename S>
+__host__ __device__ constexpr int chain_ldb(int WP) { return WP + chain_pad<S>(); }
+
 enum ChainMode { CM_PLAIN = 0, CM_AB_RIGHT = 1, CM_A_LEFT = 2, CM_B_LEFT = 3 };
 
 template <typename S>
@@ -59,11 +74,17 @@ struct ChainParams {
     // tile row instead of w^2 (real fp64, single windows; wy = 0: dense blocks)
     int wy;
     int QP;  // q rounded up to 16
+    // CM_PLAIN tiles (Q, Z: every entry read and written once per group, next touched a group later)
+    // load and store with an L2 evict-first policy, so that the side-stream Q/Z traffic does not push
+    // the chase's band and the window blocks out of L2 (HT_QZ_STREAM=0: default policy)
+    int stream_plain = 0;
 };
 
-__host__ __device__ constexpr int chain_wy_ldy(int QP) { return QP + 8; }
+template <typename S>
+__host__ __device__ constexpr int chain_wy_ldy(int QP) { return QP + chain_pad<S>(); }
+template <typename S>
 __host__ __device__ constexpr size_t chain_wy_stride(int WP, int QP) {  // scalars per window in WY layout
-    return (size_t)WP * chain_wy_ldy(QP) + (size_t)QP * (WP + 8);
+    return (size_t)WP * chain_wy_ldy<S>(QP) + (size_t)QP * chain_ldb<S>(WP);
 }
 
 // H/T chains are latency-bound by their longest tiles (right updates: the top row tiles walk
@@ -88,13 +109,13 @@ __device__ __forceinline__ void chain_order(int b, int total, int spread, bool l
 constexpr int CH_BM = 32;      // tile rows per CTA (one warp row of 4 m8 tiles)
 constexpr int CH_KC = 16;      // k rows per ring chunk
 constexpr int CH_STAGES = 3;   // ring depth
-constexpr int CH_LDX = CH_BM + 8;  // smem column stride of X (== 8 mod 16: conflict-free)
+template <typename S>
+__host__ __device__ constexpr int chain_ldx() { return CH_BM + chain_pad<S>(); }  // smem column stride of X
 #ifndef HT_STAIR_BZ
 #define HT_STAIR_BZ 4
 #endif
 constexpr int CH_SBZ = HT_STAIR_BZ;  // staircase reflectors per compact-WY block
 
-__host__ __device__ constexpr int chain_ldb(int WP) { return WP + 8; }
 // warps along the window's columns: each warp owns WP/WN columns (a multiple of 8)
 __host__ __device__ constexpr int chain_wn(int WP) { return (WP % 64 == 0) ? 8 : 4; }
 // warps along the tile rows: 8 warps per CTA (the chains are latency-bound; a warp's DMMA
@@ -105,13 +126,13 @@ __host__ __device__ constexpr int chain_wn(int WP) { return (WP % 64 == 0) ? 8 :
 __host__ __device__ constexpr int chain_wm(int WP) { return chain_wn(WP) == 8 ? 1 : HT_CHAIN_WM; }
 __host__ __device__ constexpr int chain_nt(int WP) { return 32 * chain_wn(WP) * chain_wm(WP); }
 
-// dynamic smem: [64 B mbarriers][circular X: (w+r) x CH_LDX][block ring][staircase refl.]
+// dynamic smem: [64 B mbarriers][circular X: (w+r) x chain_ldx][block ring][staircase refl.]
 template <typename S, int WP>
 __host__ __device__ constexpr size_t chain_smem_bytes(int r, int q, int P = 1, int QP = 0) {
-    return 64 + (size_t)(P > 1 ? q + 2 * P * r - 1 : q + r - 1 + r) * CH_LDX * sizeof(S) +
-           (size_t)CH_STAGES * CH_KC * chain_ldb(WP) * sizeof(S) + (size_t)(q + 1) * (r + 1) * sizeof(S) +
+    return 64 + (size_t)(P > 1 ? q + 2 * P * r - 1 : q + r - 1 + r) * chain_ldx<S>() * sizeof(S) +
+           (size_t)CH_STAGES * CH_KC * chain_ldb<S>(WP) * sizeof(S) + (size_t)(q + 1) * (r + 1) * sizeof(S) +
            (size_t)2 * ((q + CH_SBZ - 1) / CH_SBZ) * CH_SBZ * CH_SBZ * sizeof(S) +  // staircase block factors
-           (size_t)QP * CH_LDX * sizeof(S);  // WY: the tile's X Y (QP columns)
+           (size_t)QP * chain_ldx<S>() * sizeof(S);  // WY: the tile's X Y (QP columns)
 }
 
 // ---- PTX helpers ---------------------------------------------------------------------
@@ -128,6 +149,26 @@ template <typename S>
 __device__ __forceinline__ void cp_async_elem(S* s, const S* g) {
     if constexpr (sizeof(S) == 8) cp_async8(s, g);
     else cp_async16(s, g);
+}
+__device__ __forceinline__ unsigned long long l2_evict_first_policy() {
+    unsigned long long pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol));
+    return pol;
+}
+template <typename S>
+__device__ __forceinline__ void cp_async_elem_hint(S* s, const S* g, unsigned long long pol) {
+    if constexpr (sizeof(S) == 8)
+        asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 8, %2;\n" ::"r"(smem_u32(s)), "l"(g), "l"(pol));
+    else
+        asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n" ::"r"(smem_u32(s)), "l"(g), "l"(pol));
+}
+template <typename S>
+__device__ __forceinline__ void st_hint(S* g, const S& v, unsigned long long pol) {
+    if constexpr (sizeof(S) == 8) {
+        asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;\n" ::"l"(g), "d"(v), "l"(pol) : "memory");
+    } else {
+        asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;\n" ::"l"(g), "d"(v.x), "d"(v.y), "l"(pol) : "memory");
+    }
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
@@ -199,7 +240,8 @@ __device__ __forceinline__ S maybe_conj(S x, bool c) {
 // ring's mbarriers.
 template <typename S, int WP>
 __device__ __forceinline__ bool chain_tile(const ChainParams<S>& P, int bid, unsigned char* smraw, int grp, int gbar) {
-    constexpr int LDB = chain_ldb(WP);
+    constexpr int LDB = chain_ldb<S>(WP);
+    constexpr int CH_LDX = chain_ldx<S>();
     constexpr int CH_NT = chain_nt(WP);
     constexpr int NW = CH_NT / 32;
     constexpr int WN = chain_wn(WP);
@@ -241,7 +283,7 @@ __device__ __forceinline__ bool chain_tile(const ChainParams<S>& P, int bid, uns
     S* zsm = ring + (size_t)CH_STAGES * CH_KC * LDB;
     // WY: the tile's A = X Y (QP columns x CH_LDX), after the staircase records and factors
     const bool WYm = P.wy != 0;
-    const int QPw = P.QP, LDY = chain_wy_ldy(P.QP);
+    const int QPw = P.QP, LDY = chain_wy_ldy<S>(P.QP);
     S* Abuf = zsm + (size_t)(qp + 1) * (r + 1) + (size_t)2 * ((qp + CH_SBZ - 1) / CH_SBZ) * CH_SBZ * CH_SBZ;
 
     // ---- window range of this tile ----
@@ -277,7 +319,7 @@ __device__ __forceinline__ bool chain_tile(const ChainParams<S>& P, int bid, uns
         return full ? glo : khi;
     };
     auto step_blk = [&](int khi, int klo) -> const S* {
-        if (WYm) return J.Blk + (size_t)khi * chain_wy_stride(WP, QPw);
+        if (WYm) return J.Blk + (size_t)khi * chain_wy_stride<S>(WP, QPw);
         return klo < khi ? J.MBlk + ((size_t)(klo / PM) * WP) * LDB : J.Blk + ((size_t)khi * WP) * LDB;
     };
     auto step_w = [&](int khi, int klo) { return min(qp + (khi - klo + 1) * r - 1, n - (j1 + klo * r + 1) + 1); };
@@ -296,12 +338,17 @@ __device__ __forceinline__ bool chain_tile(const ChainParams<S>& P, int bid, uns
     };
     // load chain indices [c0, c0+cnt) into circular positions starting at p (cp.async)
     // (lanes run along the contiguous direction of the global matrix; no integer division)
+    const bool hint = mode == CM_PLAIN && P.stream_plain != 0;
+    const unsigned long long pol = hint ? l2_evict_first_policy() : 0ull;
     auto load_cols = [&](int c0, int cnt, int p) {
         if (!trans) {
             for (int l = warp; l < cnt; l += NW) {
                 int pos = p + l;
                 if (pos >= CIRC) pos -= CIRC;
-                for (int i = lane; i < nr; i += 32) cp_async_elem(&X[pos * CH_LDX + i], gptr(R0 + i, c0 + l));
+                if (hint)
+                    for (int i = lane; i < nr; i += 32) cp_async_elem_hint(&X[pos * CH_LDX + i], gptr(R0 + i, c0 + l), pol);
+                else
+                    for (int i = lane; i < nr; i += 32) cp_async_elem(&X[pos * CH_LDX + i], gptr(R0 + i, c0 + l));
             }
         } else {
             for (int i = warp; i < nr; i += NW)
@@ -317,7 +364,10 @@ __device__ __forceinline__ bool chain_tile(const ChainParams<S>& P, int bid, uns
             for (int l = warp; l < cnt; l += NW) {
                 int pos = p + l;
                 if (pos >= CIRC) pos -= CIRC;
-                for (int i = lane; i < nr; i += 32) *gptr(R0 + i, c0 + l) = X[pos * CH_LDX + i];
+                if (hint)
+                    for (int i = lane; i < nr; i += 32) st_hint(gptr(R0 + i, c0 + l), X[pos * CH_LDX + i], pol);
+                else
+                    for (int i = lane; i < nr; i += 32) *gptr(R0 + i, c0 + l) = X[pos * CH_LDX + i];
             }
         } else {
             for (int i = warp; i < nr; i += NW)

@@ -288,6 +288,7 @@ struct Plan {
     int P = 1;        // window merge factor of the apply chains (K2m)
     int nsm = 148;    // SMs (longest-chain-first tile order of the H/T chains)
     bool qz_late = true;   // Q/Z chains of a group start after its H/T chains (HT_QZ_LATE=0: after K2)
+    int qz_stream = 0;     // Q/Z tiles loaded / stored with an L2 evict-first policy (HT_QZ_STREAM)
     bool qz_groups = false;  // Q/Z chains as two tile groups per CTA (chain_kernel2; HT_QZ_GROUPS=0: off)
     bool far_side = false;   // one GPU: far H/T tiles' right updates on the side stream (HT_FAR_SIDE)
     int wy = 0, QP = 0;      // WY window blocks (chain.cuh ChainParams::wy; accum_wy_kernel)
@@ -301,7 +302,7 @@ struct Plan {
     bool is_root() const { return comm == nullptr || rank == root; }
     bool qz() const { return Q || Z; }
     bool same(const Plan& o) const {
-        return n == o.n && r == o.r && q == o.q && strip_cap == o.strip_cap && helpers == o.helpers && P == o.P && qz_late == o.qz_late && qz_groups == o.qz_groups && far_side == o.far_side && wy == o.wy && hlag == o.hlag && rqu == o.rqu && hbal == o.hbal && hF == o.hF && rqu_self_num == o.rqu_self_num && rqu_self_den == o.rqu_self_den && G == o.G && emul_ht == o.emul_ht && gate == o.gate && H == o.H && ldh == o.ldh &&
+        return n == o.n && r == o.r && q == o.q && strip_cap == o.strip_cap && helpers == o.helpers && P == o.P && qz_late == o.qz_late && qz_stream == o.qz_stream && qz_groups == o.qz_groups && far_side == o.far_side && wy == o.wy && hlag == o.hlag && rqu == o.rqu && hbal == o.hbal && hF == o.hF && rqu_self_num == o.rqu_self_num && rqu_self_den == o.rqu_self_den && G == o.G && emul_ht == o.emul_ht && gate == o.gate && H == o.H && ldh == o.ldh &&
                T == o.T && ldt == o.ldt && Q == o.Q && ldq == o.ldq && Z == o.Z && ldz == o.ldz;
     }
 };
@@ -764,8 +765,9 @@ int enqueue_groups(const Plan<S>& p, Workspace<S>& ws, cudaStream_t stream, bool
                                                     {p.Z, p.ldz, ws.V[bsel], ws.MV[bsel], CM_PLAIN, 0, nt, t0}},
                                   (p.Q && p.Z) ? 2 : 1, ws.Zr, p.P};
                 pq.gate = p.gate;
-            pq.wy = p.wy;
-            pq.QP = p.QP;
+                pq.wy = p.wy;
+                pq.QP = p.QP;
+                pq.stream_plain = p.qz_stream;
                 // persistent grid leaving q whole SMs: the chase of the next group starts at once
                 if (p.qz_groups) {
                     if (int rc = chain2<S>(pq, WP, std::min((pq.njobs * nt + 1) / 2, p.qz_ctas), r, q, ws.side)) return rc;
@@ -1027,7 +1029,7 @@ int run(int64_t n64, int64_t r64, S* H, int64_t ldh, S* T, int64_t ldt, S* Q, in
         }
     const int Wm = q + PM * r - 1;
     const int WP = (Wm + 31) / 32 * 32;  // padded window order (DMMA tiles, ring chunks)
-    const int LDB = chain_ldb(WP);
+    const int LDB = chain_ldb<S>(WP);
     const int Kmax = 1 + (n - 1 - 2) / r;
     // shared memory of a chase CTA; what the fixed buffers leave goes to staged strip rows
     // (HT_CHASE_SMEM_KB overrides; 224 KB measured no faster than 200 at r = 32, 64)
@@ -1058,12 +1060,14 @@ int run(int64_t n64, int64_t r64, S* H, int64_t ldh, S* T, int64_t ldt, S* Q, in
     // WY window blocks: real fp64, q in (16, 32] (QP = 32), single windows (no
     // K2m), 4 warp columns.  A step costs 2 w QP MACs per tile row instead of w^2 (w = q + r - 1), but
     // runs two GEMMs with a shared-memory hand-off: measured config 5 (w = 159) 103.1 -> 95.8 s per
-    // call, config 4 (w = 95) 10.88 -> 12.47 s -- on for r >= 128 (HT_WY=0/1 overrides)
+    // call; config 4 (w = 95) 10.88 -> 12.47 s with the old shared-memory strides (two-way bank
+    // conflicts on every fragment load, which the thin GEMMs feel most) and 7.85 -> 7.73 s with the
+    // conflict-free ones -- on for r >= 64 (HT_WY=0/1 overrides)
     int wy = 0;
     {
         const bool feasible = sizeof(S) == 8 && PM == 1 && q > 16 && q <= 32 && chain_wn(WP) == 4;
         const char* e = getenv("HT_WY");
-        wy = feasible && (e ? atoi(e) != 0 : r >= 128);
+        wy = feasible && (e ? atoi(e) != 0 : r >= 64);
     }
     const int QPw = wy ? 32 : 0;
     const size_t ch_bytes = chain_bytes_rt<S>(WP, r, q, PM, QPw);
@@ -1101,6 +1105,9 @@ int run(int64_t n64, int64_t r64, S* H, int64_t ldh, S* T, int64_t ldt, S* Q, in
     pl.hlag = getenv("HT_HELPER_LAG") ? (atoi(getenv("HT_HELPER_LAG")) == 0 ? 0 : 1) : (r >= 32 ? 0 : 1);
     // (measured: configs 2 / 3 / 4 -0.8 / -0.3 / -1.1 % per step; HT_QZ_LATE=0 restores the early start)
     pl.qz_late = !(getenv("HT_QZ_LATE") && atoi(getenv("HT_QZ_LATE")) == 0);
+    // (measured with the conflict-free chain strides: config 4 7.85 -> 7.75 s per call, the chase beside it
+    // 5.18 -> 5.08 s; config 3 -0.4 %)
+    pl.qz_stream = getenv("HT_QZ_STREAM") ? atoi(getenv("HT_QZ_STREAM")) != 0 : 1;
     // two tile groups per Q/Z CTA where both groups' shared memory fits (one CTA per SM either way)
     pl.qz_groups = 2 * ((ch_bytes + 127) / 128 * 128) <= (size_t)smem_optin &&
                    !(getenv("HT_QZ_GROUPS") && atoi(getenv("HT_QZ_GROUPS")) == 0);
