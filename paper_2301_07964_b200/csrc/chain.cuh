@@ -78,10 +78,6 @@ struct ChainParams {
     // load and store with an L2 evict-first policy, so that the side-stream Q/Z traffic does not push
     // the chase's band and the window blocks out of L2 (HT_QZ_STREAM=0: default policy)
     int stream_plain = 0;
-    // H/T right updates with ChaseArgs::defer_far: the generate phase left the rows above b0(k-1)
-    // of window k's columns alone, so they are block rows here (rows <= j1 + (k-1) r get V_k); the
-    // staircase keeps the rows [b0(k-1), b0(k)) only
-    int defer_far = 0;
 };
 
 template <typename S>
@@ -459,7 +455,7 @@ __device__ __forceinline__ bool chain_tile(const ChainParams<S>& P, int bid, uns
             if (pn < 0) pn += CIRC;
             load_cols(c0 - shift, shift, pn);
         }
-        const int i5s = j1 + 1 + max(0, (k - (P.defer_far ? min(1, qp - 1) : qp - 1)) * r);  // first staircase row
+        const int i5s = j1 + 1 + max(0, (k - qp + 1) * r);
         const bool stair = !merged && mode == CM_AB_RIGHT && qp >= 2 && max(i5s, R0) <= min(rowmax(k), R1);
         if (stair) {
             const S* src = P.Zr + (size_t)k * (r + 1);
@@ -576,7 +572,7 @@ __device__ __forceinline__ bool chain_tile(const ChainParams<S>& P, int bid, uns
         tick(1);
         // ---- epilogue: write Y back in place for the rows the mode updates ----
         const int ylo = (!merged && (mode == CM_A_LEFT || mode == CM_B_LEFT)) ? cstart(k) : 0;
-        const int yhi = (!merged && mode == CM_AB_RIGHT) ? i5s - 1 : 0x7fffffff;
+        const int yhi = (!merged && mode == CM_AB_RIGHT) ? j1 + max(0, (k - qp + 1) * r) : 0x7fffffff;
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt) {
             const int row = rowb + mt * 8;

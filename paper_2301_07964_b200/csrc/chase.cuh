@@ -71,12 +71,6 @@ struct ChaseArgs {
     // critical resource at config 4: a helper's strip item plus its hand-overs outlast a sweep
     // step) to the sweep (HT_RQU_SELF=num/den; 0/1: none)
     int rqu_self_num = 0, rqu_self_den = 1;
-    // q <= r + 1: no step of the group reads rows above b0(k-1) of window k's columns (sweep t' > t
-    // reaches those columns only in its window k-1, rows >= b0(k-1); its window k-2 ends r + 1 - (t' - t)
-    // columns before them), so the right reflectors of those rows wait for the apply phase, where the
-    // rows get the whole window block V_k (chain.cuh, ChainParams::defer_far) instead of one
-    // reflector at a time from the far-strip helpers (HT_DEFER_FAR=0: the helpers update them)
-    int defer_far = 0;
 };
 
 // shared-memory buffers of the RQ update (chase_kernel carves them; helpers use them too)
@@ -798,7 +792,7 @@ __device__ __forceinline__ void far_strip_helper(const ChaseArgs<S>& a, int t, i
         const int i1 = j + k * r + 1;
         const int i2 = min(j + (k + 1) * r, n);
         const int i3 = min(j + (k + 2) * r, n);
-        const int i4 = max(j1 + 1 + max(0, (k + t - qp + 1) * r), a.defer_far ? j1 + (k - 1) * r + 1 : 0);
+        const int i4 = j1 + 1 + max(0, (k + t - qp + 1) * r);
         const int m = i2 - i1 + 1;
         const int cF = j1 + (k - a.hlag) * r + 1;  // rows above b0(k - lag) (see above)
         const int nAf = max(0, min(cF, i3 + 1) - i4), nBf = max(0, min(cF, i2 + 1) - i4);
@@ -1108,7 +1102,7 @@ __global__ void __launch_bounds__(NT, 1) chase_kernel(ChaseArgs<S> a) {
         const int i3 = min(j + (k + 2) * r, n);
         const int i4g = j1 + 1 + max(0, (k + t - qp + 1) * r);
         // this CTA's part of the band: rows >= b0(k-1) when the helpers take the far rows
-        const int i4 = a.helpers ? max(i4g, j1 + (k - a.hlag) * r + 1) : (a.defer_far ? max(i4g, j1 + (k - 1) * r + 1) : i4g);
+        const int i4 = a.helpers ? max(i4g, j1 + (k - a.hlag) * r + 1) : i4g;
         const int b0 = j1 + k * r + 1;
         const int m = i2 - i1 + 1;
         const int L = (t > 0) ? min(j - 1 + (k + 1) * r, n) - b0 + 1 : 0;

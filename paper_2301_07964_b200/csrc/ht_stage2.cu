@@ -289,7 +289,6 @@ struct Plan {
     int nsm = 148;    // SMs (longest-chain-first tile order of the H/T chains)
     bool qz_late = true;   // Q/Z chains of a group start after its H/T chains (HT_QZ_LATE=0: after K2)
     int qz_stream = 0;     // Q/Z tiles loaded / stored with an L2 evict-first policy (HT_QZ_STREAM)
-    int defer_far = 0;     // q <= r + 1: the far band rows wait for the apply phase (ChaseArgs::defer_far)
     bool qz_groups = false;  // Q/Z chains as two tile groups per CTA (chain_kernel2; HT_QZ_GROUPS=0: off)
     bool far_side = false;   // one GPU: far H/T tiles' right updates on the side stream (HT_FAR_SIDE)
     int wy = 0, QP = 0;      // WY window blocks (chain.cuh ChainParams::wy; accum_wy_kernel)
@@ -303,7 +302,7 @@ struct Plan {
     bool is_root() const { return comm == nullptr || rank == root; }
     bool qz() const { return Q || Z; }
     bool same(const Plan& o) const {
-        return n == o.n && r == o.r && q == o.q && strip_cap == o.strip_cap && helpers == o.helpers && P == o.P && qz_late == o.qz_late && qz_stream == o.qz_stream && defer_far == o.defer_far && qz_groups == o.qz_groups && far_side == o.far_side && wy == o.wy && hlag == o.hlag && rqu == o.rqu && hbal == o.hbal && hF == o.hF && rqu_self_num == o.rqu_self_num && rqu_self_den == o.rqu_self_den && G == o.G && emul_ht == o.emul_ht && gate == o.gate && H == o.H && ldh == o.ldh &&
+        return n == o.n && r == o.r && q == o.q && strip_cap == o.strip_cap && helpers == o.helpers && P == o.P && qz_late == o.qz_late && qz_stream == o.qz_stream && qz_groups == o.qz_groups && far_side == o.far_side && wy == o.wy && hlag == o.hlag && rqu == o.rqu && hbal == o.hbal && hF == o.hF && rqu_self_num == o.rqu_self_num && rqu_self_den == o.rqu_self_den && G == o.G && emul_ht == o.emul_ht && gate == o.gate && H == o.H && ldh == o.ldh &&
                T == o.T && ldt == o.ldt && Q == o.Q && ldq == o.ldq && Z == o.Z && ldz == o.ldz;
     }
 };
@@ -634,7 +633,6 @@ int enqueue_groups(const Plan<S>& p, Workspace<S>& ws, cudaStream_t stream, bool
             ca.Fdone = ws.Fdone;
             ca.rqu_self_num = p.rqu_self_num;
             ca.rqu_self_den = p.rqu_self_den;
-            ca.defer_far = p.defer_far;
             const size_t lag_elems = (size_t)2 * qp * K * (1 + p.helpers);
             if (ws.lag) CK(cudaMemsetAsync(ws.lag, 0, lag_elems * sizeof(unsigned long long), stream));
             void* kargs[] = {&ca};
@@ -700,7 +698,6 @@ int enqueue_groups(const Plan<S>& p, Workspace<S>& ws, cudaStream_t stream, bool
             ChainParams<S> pf{n, r, qp, j1, K, {{p.H, p.ldh, ws.V[bsel], ws.MV[bsel], CM_AB_RIGHT, 0, nf, 0},
                                                 {p.T, p.ldt, ws.V[bsel], ws.MV[bsel], CM_AB_RIGHT, 0, nf, 0}}, 2, ws.Zr, p.P, 0};
             pf.gate = p.gate;
-            pf.defer_far = p.defer_far;
             pf.wy = p.wy;
             pf.QP = p.QP;
             if (p.qz_groups) {
@@ -726,7 +723,6 @@ int enqueue_groups(const Plan<S>& p, Workspace<S>& ws, cudaStream_t stream, bool
                                                     {Tk, ltk, ws.V[bsel], ws.MV[bsel], CM_AB_RIGHT, 0, cnt, rk, p.G}}, 2, ws.Zr, p.P,
                                   0};
                 pf.gate = p.gate;
-            pf.defer_far = p.defer_far;
             pf.wy = p.wy;
             pf.QP = p.QP;
                 if (int rc = chain<S>(pf, WP, 2 * cnt, r, q, stream)) return rc;
@@ -739,7 +735,6 @@ int enqueue_groups(const Plan<S>& p, Workspace<S>& ws, cudaStream_t stream, bool
                               getenv("HT_CHAIN_PROF_TILE") ? atoi(getenv("HT_CHAIN_PROF_TILE")) : 0,
                               !(getenv("HT_STAIR_FIRST") && atoi(getenv("HT_STAIR_FIRST")) == 0)};
             pr.gate = p.gate;
-            pr.defer_far = p.defer_far;
             pr.wy = p.wy;
             pr.QP = p.QP;
             if (int rc = chain<S>(pr, WP, 2 * (tiles - nf), r, q, stream)) return rc;
@@ -1113,7 +1108,6 @@ int run(int64_t n64, int64_t r64, S* H, int64_t ldh, S* T, int64_t ldt, S* Q, in
     // (measured with the conflict-free chain strides: config 4 7.85 -> 7.75 s per call, the chase beside it
     // 5.18 -> 5.08 s; config 3 -0.4 %)
     pl.qz_stream = getenv("HT_QZ_STREAM") ? atoi(getenv("HT_QZ_STREAM")) != 0 : 1;
-    pl.defer_far = q <= r + 1 && !(getenv("HT_DEFER_FAR") && atoi(getenv("HT_DEFER_FAR")) == 0);
     // two tile groups per Q/Z CTA where both groups' shared memory fits (one CTA per SM either way)
     pl.qz_groups = 2 * ((ch_bytes + 127) / 128 * 128) <= (size_t)smem_optin &&
                    !(getenv("HT_QZ_GROUPS") && atoi(getenv("HT_QZ_GROUPS")) == 0);
