@@ -78,6 +78,7 @@ struct ChainParams {
     // load and store with an L2 evict-first policy, so that the side-stream Q/Z traffic does not push
     // the chase's band and the window blocks out of L2 (HT_QZ_STREAM=0: default policy)
     int stream_plain = 0;
+    int tmap = 0;  // transposed tiles (left updates): 4 x 8 lane map of the tile loads / stores (HT_CHAIN_TMAP)
 };
 
 template <typename S>
@@ -351,6 +352,20 @@ __device__ __forceinline__ bool chain_tile(const ChainParams<S>& P, int bid, uns
                     for (int i = lane; i < nr; i += 32) cp_async_elem(&X[pos * CH_LDX + i], gptr(R0 + i, c0 + l));
             }
         } else {
+            if (P.tmap) {
+                // 4 consecutive chain indices (32 B of one matrix column) x 8 tile rows per warp
+                // instruction: conflict-free in shared memory with the strides above (a warp along
+                // the chain index alone writes with stride CH_LDX: four-way conflicts)
+                const int ngl = (cnt + 3) >> 2;
+                for (int u = warp; u < 4 * ngl; u += NW) {
+                    const int i = (u & 3) * 8 + (lane >> 2), l = (u >> 2) * 4 + (lane & 3);
+                    if (i < nr && l < cnt) {
+                        int pos = p + l;
+                        if (pos >= CIRC) pos -= CIRC;
+                        cp_async_elem(&X[pos * CH_LDX + i], gptr(R0 + i, c0 + l));
+                    }
+                }
+            } else
             for (int i = warp; i < nr; i += NW)
                 for (int l = lane; l < cnt; l += 32) {
                     int pos = p + l;
@@ -370,6 +385,17 @@ __device__ __forceinline__ bool chain_tile(const ChainParams<S>& P, int bid, uns
                     for (int i = lane; i < nr; i += 32) *gptr(R0 + i, c0 + l) = X[pos * CH_LDX + i];
             }
         } else {
+            if (P.tmap) {
+                const int ngl = (cnt + 3) >> 2;
+                for (int u = warp; u < 4 * ngl; u += NW) {
+                    const int i = (u & 3) * 8 + (lane >> 2), l = (u >> 2) * 4 + (lane & 3);
+                    if (i < nr && l < cnt) {
+                        int pos = p + l;
+                        if (pos >= CIRC) pos -= CIRC;
+                        *gptr(R0 + i, c0 + l) = X[pos * CH_LDX + i];
+                    }
+                }
+            } else
             for (int i = warp; i < nr; i += NW)
                 for (int l = lane; l < cnt; l += 32) {
                     int pos = p + l;

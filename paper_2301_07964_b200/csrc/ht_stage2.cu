@@ -289,6 +289,7 @@ struct Plan {
     int nsm = 148;    // SMs (longest-chain-first tile order of the H/T chains)
     bool qz_late = true;   // Q/Z chains of a group start after its H/T chains (HT_QZ_LATE=0: after K2)
     int qz_stream = 0;     // Q/Z tiles loaded / stored with an L2 evict-first policy (HT_QZ_STREAM)
+    int tmap = 0;          // left-update tiles: conflict-free 4 x 8 lane map of the loads / stores (HT_CHAIN_TMAP)
     bool qz_groups = false;  // Q/Z chains as two tile groups per CTA (chain_kernel2; HT_QZ_GROUPS=0: off)
     bool far_side = false;   // one GPU: far H/T tiles' right updates on the side stream (HT_FAR_SIDE)
     int wy = 0, QP = 0;      // WY window blocks (chain.cuh ChainParams::wy; accum_wy_kernel)
@@ -302,7 +303,7 @@ struct Plan {
     bool is_root() const { return comm == nullptr || rank == root; }
     bool qz() const { return Q || Z; }
     bool same(const Plan& o) const {
-        return n == o.n && r == o.r && q == o.q && strip_cap == o.strip_cap && helpers == o.helpers && P == o.P && qz_late == o.qz_late && qz_stream == o.qz_stream && qz_groups == o.qz_groups && far_side == o.far_side && wy == o.wy && hlag == o.hlag && rqu == o.rqu && hbal == o.hbal && hF == o.hF && rqu_self_num == o.rqu_self_num && rqu_self_den == o.rqu_self_den && G == o.G && emul_ht == o.emul_ht && gate == o.gate && H == o.H && ldh == o.ldh &&
+        return n == o.n && r == o.r && q == o.q && strip_cap == o.strip_cap && helpers == o.helpers && P == o.P && qz_late == o.qz_late && qz_stream == o.qz_stream && tmap == o.tmap && qz_groups == o.qz_groups && far_side == o.far_side && wy == o.wy && hlag == o.hlag && rqu == o.rqu && hbal == o.hbal && hF == o.hF && rqu_self_num == o.rqu_self_num && rqu_self_den == o.rqu_self_den && G == o.G && emul_ht == o.emul_ht && gate == o.gate && H == o.H && ldh == o.ldh &&
                T == o.T && ldt == o.ldt && Q == o.Q && ldq == o.ldq && Z == o.Z && ldz == o.ldz;
     }
 };
@@ -743,6 +744,7 @@ int enqueue_groups(const Plan<S>& p, Workspace<S>& ws, cudaStream_t stream, bool
                               chain_spread(p.nsm), ws.k1prof ? ws.k1prof + 32 : nullptr,
                               getenv("HT_CHAIN_PROF_TILE") ? atoi(getenv("HT_CHAIN_PROF_TILE")) : 0};
             pl.gate = p.gate;
+            pl.tmap = p.tmap;
             pl.wy = p.wy;
             pl.QP = p.QP;
             if (int rc = chain<S>(pl, WP, 2 * tiles, r, q, stream)) return rc;
@@ -1108,6 +1110,7 @@ int run(int64_t n64, int64_t r64, S* H, int64_t ldh, S* T, int64_t ldt, S* Q, in
     // (measured with the conflict-free chain strides: config 4 7.85 -> 7.75 s per call, the chase beside it
     // 5.18 -> 5.08 s; config 3 -0.4 %)
     pl.qz_stream = getenv("HT_QZ_STREAM") ? atoi(getenv("HT_QZ_STREAM")) != 0 : 1;
+    pl.tmap = getenv("HT_CHAIN_TMAP") ? atoi(getenv("HT_CHAIN_TMAP")) != 0 : 0;
     // two tile groups per Q/Z CTA where both groups' shared memory fits (one CTA per SM either way)
     pl.qz_groups = 2 * ((ch_bytes + 127) / 128 * 128) <= (size_t)smem_optin &&
                    !(getenv("HT_QZ_GROUPS") && atoi(getenv("HT_QZ_GROUPS")) == 0);
