@@ -1110,6 +1110,7 @@ int run(int64_t n64, int64_t r64, S* H, int64_t ldh, S* T, int64_t ldt, S* Q, in
     // (measured with the conflict-free chain strides: config 4 7.85 -> 7.75 s per call, the chase beside it
     // 5.18 -> 5.08 s; config 3 -0.4 %)
     pl.qz_stream = getenv("HT_QZ_STREAM") ? atoi(getenv("HT_QZ_STREAM")) != 0 : 1;
+    // (measured a wash: config 4 H/T 2.60 -> 2.65 s, config 3 1.224 -> 1.209 s; off)
     pl.tmap = getenv("HT_CHAIN_TMAP") ? atoi(getenv("HT_CHAIN_TMAP")) != 0 : 0;
     // two tile groups per Q/Z CTA where both groups' shared memory fits (one CTA per SM either way)
     pl.qz_groups = 2 * ((ch_bytes + 127) / 128 * 128) <= (size_t)smem_optin &&
