@@ -143,6 +143,15 @@ int ht_slab_range(int64_t n, int nranks, int rank, int64_t *row0, int64_t *nrows
  * that never become far: *owner = *group = *col0 = -1.  Host-only; returns 0 or -i. */
 int ht_far_tile_plan(int64_t n, int64_t q, int nranks, int64_t tile, int *owner, int64_t *group, int64_t *col0);
 
+/* Shared-memory strides of the K3/K4 chain kernels ("Chain shared-memory
+ * strides"), in elements of the scalar type: *ldx = stride between chain columns of the tile buffer
+ * X (tile rows contiguous), *ldb = row stride of a window block of padded width wp (wp = the
+ * window width q + r - 1 rounded up to 32, 64, 96, 128 or 160).  The DMMA m8n8k4 fragment loads
+ * put lane & 3 along the stride and lane >> 2 along the contiguous direction; the strides are
+ * chosen so that such a load is bank-conflict-free (tests/test_abi.py checks this by enumeration).
+ * Host-only; returns 0 or -i for argument i. */
+int ht_chain_smem_strides(int is_complex, int wp, int *ldx, int *ldb);
+
 /* Human-readable text for a return code (static storage). */
 const char *ht_strerror(int code);
 

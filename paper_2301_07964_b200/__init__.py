@@ -79,6 +79,8 @@ def _load():
     lib.ht_far_tile_plan.argtypes = [i64, i64, ctypes.c_int, i64, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(i64),
                                      ctypes.POINTER(i64)]
     lib.ht_far_tile_plan.restype = ctypes.c_int
+    lib.ht_chain_smem_strides.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)]
+    lib.ht_chain_smem_strides.restype = ctypes.c_int
     lib.ht_release_cache.argtypes = []
     lib.ht_release_cache.restype = ctypes.c_int
     _lib = lib
@@ -88,13 +90,23 @@ def _load():
 EXPORTED_SYMBOLS = ("ht_stage2_d", "ht_stage2_z", "ht_stage2_d_ex", "ht_stage2_z_ex",
                     "ht_nccl_unique_id", "ht_comm_create", "ht_comm_destroy", "ht_slab_range", "ht_strerror",
                     "ht_flops_std", "ht_default_q", "ht_last_timing", "ht_probe_dmma_tflops",
-                    "ht_probe_dfma_tflops", "ht_release_cache", "ht_last_lag_check", "ht_far_tile_plan")
+                    "ht_probe_dfma_tflops", "ht_release_cache", "ht_last_lag_check", "ht_far_tile_plan",
+                    "ht_chain_smem_strides")
 
 
 def slab_range(n: int, nranks: int, rank: int):
     """(row0, nrows) of the Q/Z row slab rank `rank` of `nranks` updates (multi-GPU, C ABI)."""
     a, b = ctypes.c_int64(), ctypes.c_int64()
     rc = _load().ht_slab_range(int(n), int(nranks), int(rank), ctypes.byref(a), ctypes.byref(b))
+    if rc != 0:
+        raise HTError(rc)
+    return a.value, b.value
+
+
+def chain_smem_strides(is_complex: bool, wp: int):
+    """(ldx, ldb): shared-memory strides of the chain kernels in elements (C ABI ht_chain_smem_strides)."""
+    a, b = ctypes.c_int(), ctypes.c_int()
+    rc = _load().ht_chain_smem_strides(int(bool(is_complex)), int(wp), ctypes.byref(a), ctypes.byref(b))
     if rc != 0:
         raise HTError(rc)
     return a.value, b.value

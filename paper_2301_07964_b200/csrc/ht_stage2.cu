@@ -1268,6 +1268,15 @@ int ht_far_tile_plan(int64_t n, int64_t q, int nranks, int64_t tile, int* owner,
     return HT_OK;
 }
 
+int ht_chain_smem_strides(int is_complex, int wp, int* ldx, int* ldb) {
+    if (wp < 8 || wp % 8 != 0) return -2;
+    if (!ldx) return -3;
+    if (!ldb) return -4;
+    *ldx = is_complex ? chain_ldx<zc>() : chain_ldx<double>();
+    *ldb = is_complex ? chain_ldb<zc>(wp) : chain_ldb<double>(wp);
+    return HT_OK;
+}
+
 int ht_comm_destroy(ncclComm_t comm) {
     if (!comm) return HT_OK;
     return ncclCommDestroy(comm) == ncclSuccess ? HT_OK : HT_ENCCL;

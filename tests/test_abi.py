@@ -42,6 +42,32 @@ def test_library_exports_every_declared_symbol(ht):
     assert set(declared_functions()) == set(ht.EXPORTED_SYMBOLS)
 
 
+@pytest.mark.parametrize("cplx", [False, True])
+@pytest.mark.parametrize("wp", [32, 64, 96, 128, 160])
+def test_chain_fragment_loads_are_bank_conflict_free(ht, cplx, wp):
+    """DESIGN.md section 10 "Chain shared-memory strides": an m8n8k4 DMMA fragment load has lane & 3
+    along the stride and lane >> 2 along the contiguous direction.  Shared memory has 32 four-byte
+    banks; a warp's 8-byte loads are served per half-warp and its 16-byte loads per quarter-warp,
+    so within each such phase every lane must fall on its own bank group.  Enumerated here for the
+    strides the library reports (the old strides, stride = 8 mod 16 doubles, fail this check)."""
+    ldx, ldb = ht.chain_smem_strides(cplx, wp)
+    assert ldx >= 32 and ldb >= wp  # a column of X holds 32 tile rows; a block row holds wp columns
+    words = 4 if cplx else 2        # 4-byte words per element
+    phase = 8 if cplx else 16       # lanes served together
+    for ld in (ldx, ldb):
+        for first in range(0, 32, phase):
+            banks = set()
+            for lane in range(first, first + phase):
+                elem = (lane & 3) * ld + (lane >> 2)
+                banks.add(((elem * words) % 32) // words)
+            assert len(banks) == phase, (ld, first, sorted(banks))
+    # the check itself rejects the strides of rounds 1-2 (X: 32 + 8, blocks: wp + 8)
+    bad = {(((lane & 3) * 40 + (lane >> 2)) * 2 % 32) // 2 for lane in range(16)}
+    assert len(bad) < 16
+    with pytest.raises(ht.HTError):
+        ht.chain_smem_strides(cplx, 7)
+
+
 def test_host_only_entry_points(ht):
     assert ht.flops_std(1000) == 10.0 * 1000 ** 3  # PAPER.md:712 "10n^3"
     assert ht.flops_std(1000, True) == 40.0 * 1000 ** 3
