@@ -124,6 +124,29 @@ def test_config2_fullsize_vs_live_oracle():
     assert max(gaps.values()) <= FWD_TOL, gaps
 
 
+def test_config4_generator_n4096_vs_live_oracle():
+    """Config 4's generator and r = 64 (the RQ-update chase, WY blocks, default q) at n = 4096, the
+    largest n of that shape the oracle reduces in about a minute: every entry against the live oracle."""
+    import oracle
+    import paper_2301_07964_b200 as ht
+    Hn, Tn = config_pencil(4, int(os.environ.get("HT_C4GEN_N", "4096")))  # (8192: ~8 min of oracle, run by hand)
+    r = CONFIGS[4]["r"]
+    n = Hn.shape[0]
+    A, B = _colmajor(Hn), _colmajor(Tn)
+    H, T, Q, Z = _reduce(ht, A, B, r)
+    inv = _inv_dev(A, B, H, T, Q, Z)
+    h, t, q, z = (X.cpu().numpy() for X in (H, T, Q, Z))
+    del H, T, Q, Z
+    oracle.set_threads(len(os.sched_getaffinity(0)))
+    ho, to, qo, zo, _ = oracle.stage2(Hn, Tn, r)
+    a = normalize_phase(h, t, q, z)
+    b = normalize_phase(ho, to, qo, zo)
+    gaps = {nm: rel_diff(x, y) for nm, x, y in zip("HTQZ", a, b)}
+    _log({"test": "config4_generator_n4096_vs_live_oracle", "n": n, "r": r, "gap": gaps, "gpu_invariants": inv})
+    assert max(inv["eA"], inv["eB"], inv["oQ"], inv["oZ"]) <= inv["bound"], inv
+    assert max(gaps.values()) <= FWD_TOL, gaps
+
+
 @pytest.mark.parametrize("cfg", [2, 3, 4])
 def test_fullsize_vs_cached_oracle_samples(cfg):
     import paper_2301_07964_b200 as ht
